@@ -1,0 +1,239 @@
+// fk_capi.cpp — the extern "C" boundary (include/fk.h) of libfk_cuda.so.
+// C++ exceptions never cross it: every entry point returns an fk_status and
+// leaves the message / chain position in thread-local storage.
+#include <cstring>
+#include <string>
+
+#include "fk.h"
+#include "fk_core.hpp"
+#include "fk_cuda.h"
+#include "fk_exec.hpp"
+
+struct fk_iop {
+  fk::Op op;
+};
+struct fk_pipeline {
+  fk::Pipeline p;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int32_t g_pos = -1;
+
+template <class Fn>
+fk_status guard(Fn&& fn) {
+  try {
+    fn();
+    return FK_OK;
+  } catch (const fk::Error& e) {
+    g_err = e.what();
+    g_pos = e.position;
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_err = "CapacityOverflow: host allocation failed";
+    g_pos = -1;
+    return FK_E_CAPACITY_OVERFLOW;
+  } catch (const std::exception& e) {
+    g_err = std::string("InvalidArgument: ") + e.what();
+    g_pos = -1;
+    return FK_E_INVALID_ARGUMENT;
+  }
+}
+
+template <class Fn>
+fk_status build(fk_iop** out, Fn&& fn) {
+  if (!out) {
+    g_err = "InvalidArgument: null output pointer";
+    return FK_E_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  return guard([&] { *out = new fk_iop{fn()}; });
+}
+
+const fk::Op& deref(const fk_iop* op, const char* what) {
+  if (!op) fk::fail(FK_E_INVALID_ARGUMENT, std::string("null ") + what);
+  return op->op;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fk_backend_name(void) { return "cuda-sm100a"; }
+int32_t fk_abi_version(void) { return FK_ABI_VERSION; }
+const char* fk_last_error(void) { return g_err.c_str(); }
+int32_t fk_last_error_position(void) { return g_pos; }
+int32_t fk_errc_name(int32_t status, char* buf, size_t cap) {
+  const char* s = fk::errc_name(status);
+  if (buf && cap) {
+    std::strncpy(buf, s, cap - 1);
+    buf[cap - 1] = 0;
+  }
+  return int32_t(std::strlen(s));
+}
+
+uint32_t fk_bytes_per_element(uint32_t kind) { return fk::kind_ok(kind) ? fk::bpe(kind) : 0; }
+
+fk_status fk_plane_view(const fk_plane* p, uint32_t x0, uint32_t y0, uint32_t w, uint32_t h, fk_plane* out) {
+  return guard([&] {  // Plane::view, plane.cpp:91-101
+    fk::check_plane(p, "source");
+    if (!out) fk::fail(FK_E_INVALID_ARGUMENT, "null output");
+    if (w == 0 || h == 0 || uint64_t(x0) + w > p->width || uint64_t(y0) + h > p->height)
+      fk::fail(FK_E_BOUNDS_ERROR, "sub-view outside plane");
+    *out = *p;
+    out->data = static_cast<uint8_t*>(p->data) + (uint64_t(y0) * p->row_stride + x0) * fk::bpe(p->kind);
+    out->width = w;
+    out->height = h;
+  });
+}
+
+fk_status fk_op_arith(uint32_t id, uint32_t kind, const void* value, fk_iop** out) {
+  return build(out, [&] { return fk::make_arith(id, kind, value); });
+}
+fk_status fk_op_batch_arith(uint32_t id, uint32_t kind, const void* values, uint32_t n, fk_iop** out) {
+  return build(out, [&] { return fk::make_batch_arith(id, kind, values, n); });
+}
+fk_status fk_op_cast(uint32_t from, uint32_t to, fk_iop** out) {
+  return build(out, [&] { return fk::make_cast(from, to); });
+}
+fk_status fk_op_static_loop(const fk_iop* inner, uint32_t repeat, fk_iop** out) {
+  return build(out, [&] { return fk::make_static_loop(deref(inner, "inner op"), repeat); });
+}
+fk_status fk_op_read_per_thread(const fk_plane* src, fk_iop** out) {
+  return build(out, [&] {
+    fk::check_plane(src, "source");
+    return fk::make_read_per_thread(*src);
+  });
+}
+fk_status fk_op_write_per_thread(const fk_plane* dst, fk_iop** out) {
+  return build(out, [&] {
+    fk::check_plane(dst, "destination");
+    return fk::make_write_per_thread(*dst);
+  });
+}
+fk_status fk_op_crop(const fk_plane* src, const fk_crop_rect* rect, fk_iop** out) {
+  return build(out, [&] {
+    fk::check_plane(src, "source");
+    if (!rect) fk::fail(FK_E_INVALID_ARGUMENT, "null crop rect");
+    return fk::make_crop(*src, *rect);
+  });
+}
+fk_status fk_op_resize(const fk_iop* up, uint32_t w, uint32_t h, uint32_t mode, fk_iop** out) {
+  return build(out, [&] { return fk::make_resize(deref(up, "upstream read"), w, h, mode); });
+}
+fk_status fk_op_color_convert(uint32_t order, uint32_t in, fk_iop** out) {
+  return build(out, [&] { return fk::make_color_convert(order, in); });
+}
+fk_status fk_op_split_write(const fk_plane dst[3], fk_iop** out) {
+  return build(out, [&] {
+    if (!dst) fk::fail(FK_E_INVALID_ARGUMENT, "null destinations");
+    for (int i = 0; i < 3; ++i) fk::check_plane(&dst[i], "destination");
+    return fk::make_split_write(dst);
+  });
+}
+fk_status fk_op_batch_read(const fk_iop* const* inner, uint32_t n, uint32_t active, const void* def, fk_iop** out) {
+  return build(out, [&] {
+    std::vector<const fk::Op*> v;
+    for (uint32_t i = 0; i < n; ++i) v.push_back(&deref(inner ? inner[i] : nullptr, "inner read"));
+    return fk::make_batch_read(v, active, def);
+  });
+}
+fk_status fk_op_batch_write(const fk_iop* const* inner, uint32_t n, uint32_t active, fk_iop** out) {
+  return build(out, [&] {
+    std::vector<const fk::Op*> v;
+    for (uint32_t i = 0; i < n; ++i) v.push_back(&deref(inner ? inner[i] : nullptr, "inner write"));
+    return fk::make_batch_write(v, active);
+  });
+}
+fk_status fk_fold_unary_into_read(const fk_iop* read, const fk_iop* unary, fk_iop** out) {
+  return build(out, [&] { return fk::fold_unary_into_read(deref(read, "read"), deref(unary, "unary")); });
+}
+void fk_iop_free(fk_iop* op) { delete op; }
+
+uint32_t fk_iop_id(const fk_iop* op) { return op->op.id; }
+uint32_t fk_iop_kind(const fk_iop* op) { return op->op.opkind; }
+int32_t fk_iop_input_kind(const fk_iop* op) { return op->op.in_kind; }
+int32_t fk_iop_output_kind(const fk_iop* op) { return op->op.out_kind; }
+int32_t fk_iop_dims(const fk_iop* op, fk_extent3* out) {
+  if (!op->op.dims) return 0;
+  if (out) *out = *op->op.dims;
+  return 1;
+}
+
+fk_status fk_validate_chain(const fk_iop* const* ops, uint32_t n, fk_pipeline** out) {
+  if (!out) {
+    g_err = "InvalidArgument: null output pointer";
+    return FK_E_INVALID_ARGUMENT;
+  }
+  *out = nullptr;
+  return guard([&] {
+    std::vector<const fk::Op*> v;
+    for (uint32_t i = 0; i < n; ++i) {
+      if (!ops || !ops[i]) fk::fail(FK_E_INVALID_ARGUMENT, "null op", int(i));
+      v.push_back(&ops[i]->op);
+    }
+    *out = new fk_pipeline{fk::validate_chain(v)};
+  });
+}
+void fk_pipeline_free(fk_pipeline* p) { delete p; }
+
+fk_status fk_pipeline_iter_space(const fk_pipeline* p, fk_extent3* out) {
+  return guard([&] {
+    if (!p || !out) fk::fail(FK_E_INVALID_ARGUMENT, "null argument");
+    *out = p->p.space;
+  });
+}
+uint32_t fk_pipeline_compute_count(const fk_pipeline* p) { return p ? uint32_t(p->p.compute.size()) : 0; }
+
+fk_status fk_execute_fused(const fk_pipeline* p, const fk_exec_config* cfg, fk_exec_report* rep) {
+  return guard([&] {
+    if (!p) fk::fail(FK_E_INVALID_ARGUMENT, "null pipeline");
+    const fk_exec_report r = fk::execute_fused(p->p, cfg);
+    if (rep) *rep = r;
+  });
+}
+fk_status fk_execute_unfused(const fk_pipeline* p, const fk_exec_config* cfg, fk_exec_report* rep) {
+  return guard([&] {
+    if (!p) fk::fail(FK_E_INVALID_ARGUMENT, "null pipeline");
+    const fk_exec_report r = fk::execute_unfused(p->p, cfg);
+    if (rep) *rep = r;
+  });
+}
+fk_status fk_plan_memory_savings(const fk_pipeline* p, uint64_t* bytes) {  // executor.cpp:223-228
+  return guard([&] {
+    if (!p || !bytes) fk::fail(FK_E_INVALID_ARGUMENT, "null argument");
+    *bytes = fk::analytic_traffic(p->p).intermediates;
+  });
+}
+fk_status fk_schedule(const fk_extent3* sp, const fk_exec_config* cfg, uint32_t* tasks, uint64_t cap,
+                      uint64_t* count) {  // schedule, executor.cpp:52-61 (the CPU task partition)
+  return guard([&] {
+    if (!sp || !cfg || !count) fk::fail(FK_E_INVALID_ARGUMENT, "null argument");
+    fk::check_config(cfg);
+    const uint32_t chunk = uint32_t(cfg->chunk_rows);
+    uint64_t n = 0;
+    for (uint32_t z = 0; z < sp->batch; ++z)
+      for (uint32_t y = 0; y < sp->height; y += chunk) {
+        if (tasks && n < cap) {
+          tasks[3 * n] = z;
+          tasks[3 * n + 1] = y;
+          tasks[3 * n + 2] = y + chunk < sp->height ? y + chunk : sp->height;
+        }
+        ++n;
+      }
+    *count = n;
+  });
+}
+
+int32_t fk_cuda_device_info(char* buf, size_t cap) {
+  const std::string s = fk::device_info();
+  if (buf && cap) {
+    std::strncpy(buf, s.c_str(), cap - 1);
+    buf[cap - 1] = 0;
+  }
+  return FK_OK;
+}
+uint64_t fk_cuda_kernel_launch_count(void) { return fk::launch_count(); }
+
+}  // extern "C"

@@ -1,0 +1,81 @@
+// fk_devprog.hpp — the device-resident form of a validated pipeline.
+//
+// Built once per Pipeline (fk_exec.cu) and uploaded to HBM: per-plane read
+// params (the BatchRead array indexed by z, ops.cpp:369-378), per-plane write
+// params (BatchWrite, ops.cpp:437-445), and the compute program. Kernels get a
+// DPlan by value (kernel parameter space) and index the arrays by z.
+#pragma once
+
+#include <cstdint>
+
+namespace fk {
+
+// read modes, resolved on the host from SampleReadParams::resizing()/mode (ops.cpp:327-344)
+enum : uint32_t { RD_DIRECT = 0, RD_NEAREST = 1, RD_BILINEAR = 2 };
+// DSample::flags
+enum : uint32_t { SF_DEFAULT = 1u, SF_LANE_ALIGNED = 2u };
+// DWrite::flags
+enum : uint32_t { WF_ACTIVE = 1u, WF_LANE_ALIGNED = 2u, WF_STREAM = 4u };
+// write modes
+enum : uint32_t { WR_DIRECT = 0, WR_SPLIT = 1 };
+// compute op classes
+enum : uint32_t { OC_NOP = 0, OC_ARITH = 1, OC_SWAP = 2, OC_CAST = 3, OC_GRAY = 4 };
+// arith functions (same order as fk_op_id MUL..DIV)
+enum : uint32_t { AF_MUL = 0, AF_ADD = 1, AF_SUB = 2, AF_DIV = 3 };
+
+struct DSample {             // one plane's read (SampleReadParams, ops.hpp:78-91)
+  uint64_t src;              // device address of source element (0,0)
+  uint64_t pitch;            // bytes per source row
+  uint32_t x0, y0, rect_w, rect_h;
+  uint32_t out_w, out_h;
+  uint32_t kind;             // source ScalarKind
+  uint32_t mode;             // RD_*
+  uint32_t post_off, post_len;  // folded unaries (index into DPlan::post)
+  uint32_t flags;            // SF_*
+  uint32_t pad;
+};
+
+struct DWrite {              // one plane's write (WriteParams / SplitWriteParams)
+  uint64_t dst[3];
+  uint64_t pitch[3];         // bytes per destination row, per destination plane
+  uint32_t flags;            // WF_*
+  uint32_t pad;
+};
+
+struct DOp {                 // one compute op of the program
+  uint32_t cls;              // OC_*
+  uint32_t fn;               // AF_* for OC_ARITH
+  uint32_t lk_in, lk_out;    // lane kinds (FK_U8/FK_F32/FK_F64)
+  uint32_t nl;               // lanes (1 or 3)
+  uint32_t repeat;           // StaticLoop count (1 otherwise)
+  uint64_t c[3];             // raw lane constants (u8 value / f32 bits / f64 bits)
+  uint64_t per_z;            // BatchArith: device array of 24-byte Elements, else 0
+  uint32_t per_z_n;
+  uint32_t pad;
+};
+
+struct FastDiv {             // n / d for 32-bit n (Granlund-Montgomery round-up)
+  uint32_t d, m, s;
+};
+
+struct DPlan {
+  uint32_t width, height, batch;  // iteration space (flattened to height 1 when contiguous)
+  uint32_t tiles_per_row;
+  FastDiv tpr;
+  uint32_t tiles;            // tiles per plane = height * tiles_per_row
+  uint32_t n_ops;
+  const DOp* ops;            // compute program
+  const DOp* post;           // folded-unary programs referenced by DSample::post_off
+  const DSample* reads;      // batch entries; nullptr -> affine read below
+  const DWrite* writes;      // batch entries; nullptr -> affine write below
+  DSample rd;                // affine read: plane z at rd.src + z * rd_zstride
+  DWrite wr;                 // affine write: plane z at wr.dst + z * wr_zstride
+  uint64_t rd_zstride, wr_zstride;
+  uint32_t write_kind;       // element kind reaching the write op
+  uint32_t write_mode;       // WR_*
+  uint32_t def_kind;         // kind of the BatchRead default value
+  uint32_t pad;
+  uint64_t def[3];           // BatchRead default Element (ops.hpp:111), lane-encoded
+};
+
+}  // namespace fk

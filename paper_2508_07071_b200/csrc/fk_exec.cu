@@ -1,0 +1,526 @@
+// fk_exec.cu — pipeline -> device program, and the two executors.
+//
+// execute_fused (executor.cpp:63-85) becomes ONE kernel launch over the whole
+// (x, y, z) space; execute_unfused (executor.cpp:134-217) becomes one launch per
+// compute op through stream-ordered intermediates (cudaMallocAsync, freed after
+// the consuming pass) plus a final write launch — the in-repo comparator.
+// Counters follow the reference's accounting exactly (fk_core.cpp:analytic_traffic).
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+
+#include "fk_core.hpp"
+#include "fk_exec.hpp"
+#include "fk_launch.hpp"
+
+namespace fk {
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) fail(FK_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Lane-encode an Element (scalar.hpp:94-121) the way DOp::c / DPlan::def hold it.
+void encode_element(uint32_t kind, const Element& e, uint64_t (&c)[3]) {
+  c[0] = c[1] = c[2] = 0;
+  for (int l = 0; l < lanes_of(kind); ++l) {
+    switch (lane_kind(kind)) {
+      case FK_U8: c[l] = e.raw[l]; break;
+      case FK_F32: { uint32_t b; std::memcpy(&b, e.raw + 4 * l, 4); c[l] = b; break; }
+      default: { uint64_t b; std::memcpy(&b, e.raw + 8 * l, 8); c[l] = b; break; }
+    }
+  }
+}
+
+DOp arith_op(uint32_t fn, uint32_t kind, const Element& value, uint32_t repeat) {
+  DOp d{};
+  d.cls = OC_ARITH;
+  d.fn = fn;
+  d.lk_in = d.lk_out = lane_kind(kind);
+  d.nl = uint32_t(lanes_of(kind));
+  d.repeat = repeat;
+  encode_element(kind, value, d.c);
+  return d;
+}
+
+// compute_exec_block dispatch (ops.cpp:214-235) -> one device op
+DOp encode_compute(const Op& op) {
+  DOp d{};
+  const uint32_t in = uint32_t(op.in_kind), out = uint32_t(op.out_kind);
+  switch (op.id) {
+    case FK_OP_MUL: case FK_OP_ADD: case FK_OP_SUB: case FK_OP_DIV:
+      return arith_op(op.id - FK_OP_MUL, in, op.value, 1);
+    case FK_OP_BATCH_ARITH:
+      return arith_op(op.inner_id - FK_OP_MUL, in, Element{}, 1);  // per_z attached by caller
+    case FK_OP_STATIC_LOOP:  // static_loop_block, ops.cpp:200-210
+      switch (op.inner_id) {
+        case FK_OP_MUL: case FK_OP_ADD: case FK_OP_SUB: case FK_OP_DIV:
+          return arith_op(op.inner_id - FK_OP_MUL, op.value_kind, op.value, op.repeat);
+        case FK_OP_SWAP_RB:
+          d.cls = OC_SWAP;
+          d.repeat = op.repeat;
+          return d;
+        default:
+          d.cls = OC_NOP;  // kind-preserving cast: identity
+          return d;
+      }
+    case FK_OP_CAST:
+      if (in == out) { d.cls = OC_NOP; return d; }
+      d.cls = OC_CAST;
+      d.lk_in = lane_kind(in);
+      d.lk_out = lane_kind(out);
+      d.nl = uint32_t(lanes_of(in));
+      return d;
+    case FK_OP_SWAP_RB:
+      d.cls = OC_SWAP;
+      d.repeat = 1;
+      return d;
+    case FK_OP_TO_GRAY:
+      d.cls = OC_GRAY;
+      d.lk_in = lane_kind(in);
+      d.lk_out = FK_F32;
+      d.nl = 3;
+      return d;
+  }
+  fail(FK_E_INVALID_ARGUMENT, "not a compute op");
+}
+
+DOp encode_unary(const Folded& f) {
+  Op op;
+  op.id = f.id;
+  op.in_kind = int32_t(f.in);
+  op.out_kind = int32_t(f.out);
+  return encode_compute(op);
+}
+
+// The fused program: drop identities, merge runs of the same op into one
+// repeat count (semantically n-fold application, exactly what StaticLoop is).
+std::vector<DOp> compress(const std::vector<DOp>& ops) {
+  std::vector<DOp> out;
+  for (const DOp& d : ops) {
+    if (d.cls == OC_NOP) continue;
+    if (!out.empty()) {
+      DOp& b = out.back();
+      const bool same_arith = d.cls == OC_ARITH && b.cls == OC_ARITH && !d.per_z && !b.per_z && d.fn == b.fn &&
+                              d.lk_in == b.lk_in && d.nl == b.nl && std::memcmp(d.c, b.c, sizeof d.c) == 0;
+      const bool same_swap = d.cls == OC_SWAP && b.cls == OC_SWAP;
+      if ((same_arith || same_swap) && uint64_t(b.repeat) + d.repeat <= 0xffffffffull) {
+        b.repeat += d.repeat;
+        continue;
+      }
+    }
+    out.push_back(d);
+  }
+  return out;
+}
+
+uint64_t pitch_of(const fk_plane& p) { return uint64_t(p.row_stride) * bpe(p.kind); }
+
+bool lane_aligned(const fk_plane& p) {
+  const uint64_t lb = lane_bytes(p.kind);
+  return (reinterpret_cast<uintptr_t>(p.data) % lb) == 0 && (pitch_of(p) % lb) == 0;
+}
+
+template <class T>
+T* upload(const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  void* d = nullptr;
+  cuda_check(cudaMalloc(&d, v.size() * sizeof(T)), "cudaMalloc(program)");
+  cuda_check(cudaMemcpy(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice), "cudaMemcpy(program)");
+  return static_cast<T*>(d);
+}
+
+FastDiv make_fastdiv(uint32_t d) {
+  FastDiv f{d, 0, 0};
+  uint32_t s = 0;
+  while ((uint64_t(1) << s) < d) ++s;
+  f.s = s;
+  f.m = uint32_t(((uint64_t(1) << 32) * ((uint64_t(1) << s) - d)) / d + 1);
+  return f;
+}
+
+void add_kind(uint32_t k, bool& wide, int& lanes) {
+  if (lane_kind(k) == FK_F64) wide = true;
+  if (lanes_of(k) == 3) lanes = 3;
+}
+
+}  // namespace
+
+struct DeviceProgram {
+  int device = -1;
+  std::vector<DOp> ops;          // 1:1 with Pipeline::compute (unfused pass i runs ops[i])
+  DOp* d_ops = nullptr;
+  DOp* d_fops = nullptr;         // fused (compressed) program
+  uint32_t n_fops = 0;
+  DOp* d_post = nullptr;
+  DSample* d_reads = nullptr;
+  DWrite* d_writes = nullptr;
+  std::vector<void*> extra;      // BatchArith constant tables
+  std::vector<DSample> reads;    // host copies
+  bool read_flat = false, write_flat = false;
+  bool fused_wide = false;
+  int fused_lanes = 1;
+  bool read_wide = false;        // kinds touched by the read stage alone
+  int read_lanes = 1;
+  uint64_t def[3] = {0, 0, 0};
+  uint32_t def_kind = 0;
+
+  ~DeviceProgram() {
+    for (void* p : {static_cast<void*>(d_ops), static_cast<void*>(d_fops), static_cast<void*>(d_post),
+                    static_cast<void*>(d_reads), static_cast<void*>(d_writes)})
+      if (p) cudaFree(p);
+    for (void* p : extra) cudaFree(p);
+  }
+};
+
+Pipeline::~Pipeline() = default;
+
+namespace {
+
+std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
+  auto dp = std::make_shared<DeviceProgram>();
+  dp->device = device;
+  const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
+
+  // compute program (1:1) + BatchArith constant tables
+  for (const Op& op : p.compute) {
+    DOp d = encode_compute(op);
+    if (op.id == FK_OP_BATCH_ARITH) {
+      std::vector<uint64_t> rows(op.values.size() * 3);
+      for (size_t z = 0; z < op.values.size(); ++z) {
+        uint64_t c[3];
+        encode_element(uint32_t(op.in_kind), op.values[z], c);
+        std::memcpy(&rows[3 * z], c, sizeof c);
+      }
+      uint64_t* t = upload(rows);
+      dp->extra.push_back(t);
+      d.per_z = reinterpret_cast<uint64_t>(t);
+      d.per_z_n = uint32_t(op.values.size());
+    }
+    dp->ops.push_back(d);
+    add_kind(uint32_t(op.in_kind), dp->fused_wide, dp->fused_lanes);
+    add_kind(uint32_t(op.out_kind), dp->fused_wide, dp->fused_lanes);
+  }
+  const std::vector<DOp> fops = compress(dp->ops);
+  dp->n_fops = uint32_t(fops.size());
+
+  // per-plane reads (BatchRead array, ops.cpp:369-378) + deduplicated post programs
+  std::vector<DOp> post;
+  std::map<std::vector<uint32_t>, uint32_t> post_index;
+  bool flat = uint64_t(W) * H < (uint64_t(1) << 32);
+  dp->def_kind = uint32_t(p.read.out_kind);
+  if (p.read.id == FK_OP_BATCH_READ) encode_element(dp->def_kind, p.read.def, dp->def);
+  add_kind(dp->def_kind, dp->read_wide, dp->read_lanes);
+  for (uint32_t z = 0; z < B; ++z) {
+    DSample s{};
+    const Sample* sp = read_plane(p, z);
+    if (!sp) {
+      s.flags = SF_DEFAULT;
+      dp->reads.push_back(s);
+      continue;
+    }
+    s.src = reinterpret_cast<uint64_t>(sp->source.data);
+    s.pitch = pitch_of(sp->source);
+    s.x0 = sp->x0;
+    s.y0 = sp->y0;
+    s.rect_w = sp->rect_w;
+    s.rect_h = sp->rect_h;
+    s.out_w = sp->out_w;
+    s.out_h = sp->out_h;
+    s.kind = sp->source.kind;
+    s.mode = !sp->resizing() ? RD_DIRECT : (sp->mode == FK_NEAREST ? RD_NEAREST : RD_BILINEAR);
+    s.flags = lane_aligned(sp->source) ? SF_LANE_ALIGNED : 0;
+    add_kind(s.kind, dp->read_wide, dp->read_lanes);
+    if (!sp->post.empty()) {
+      std::vector<uint32_t> key;
+      for (const Folded& f : sp->post) {
+        key.insert(key.end(), {f.id, f.in, f.out});
+        add_kind(f.in, dp->read_wide, dp->read_lanes);
+        add_kind(f.out, dp->read_wide, dp->read_lanes);
+      }
+      auto it = post_index.find(key);
+      if (it == post_index.end()) {
+        const uint32_t off = uint32_t(post.size());
+        for (const Folded& f : sp->post) post.push_back(encode_unary(f));
+        it = post_index.emplace(key, off).first;
+      }
+      s.post_off = it->second;
+      s.post_len = uint32_t(sp->post.size());
+    }
+    // contiguous identity read of whole rows -> the plane is one flat run
+    flat = flat && s.mode == RD_DIRECT && s.x0 == 0 && s.y0 == 0 && sp->source.row_stride == W;
+    dp->reads.push_back(s);
+  }
+  dp->read_flat = flat;
+
+  // per-plane writes (BatchWrite array, ops.cpp:437-445)
+  std::vector<DWrite> writes;
+  const bool batch_w = p.write.id == FK_OP_BATCH_WRITE;
+  const uint32_t wid = batch_w ? p.write.w_inner : p.write.id;
+  const int per = wid == FK_OP_SPLIT_WRITE ? 3 : 1;
+  bool wflat = uint64_t(W) * H < (uint64_t(1) << 32);
+  for (uint32_t z = 0; z < B; ++z) {
+    DWrite w{};
+    const bool active = !batch_w || z < p.write.active;
+    w.flags = active ? (WF_ACTIVE | WF_STREAM) : 0;
+    bool al = true;
+    for (int l = 0; l < per; ++l) {
+      const fk_plane& d = batch_w ? p.write.wdest[size_t(z) * per + l] : p.write.dest[l];
+      w.dst[l] = reinterpret_cast<uint64_t>(d.data);
+      w.pitch[l] = pitch_of(d);
+      al = al && lane_aligned(d);
+      wflat = wflat && d.row_stride == W;
+    }
+    if (al) w.flags |= WF_LANE_ALIGNED;
+    writes.push_back(w);
+  }
+  dp->write_flat = wflat;
+  add_kind(uint32_t(p.write.in_kind), dp->fused_wide, dp->fused_lanes);
+  if (dp->read_wide) dp->fused_wide = true;
+  if (dp->read_lanes == 3) dp->fused_lanes = 3;
+
+  dp->d_ops = upload(dp->ops);
+  dp->d_fops = upload(fops);
+  dp->d_post = upload(post);
+  dp->d_reads = upload(dp->reads);
+  dp->d_writes = upload(writes);
+  return dp;
+}
+
+DPlan base_plan(uint32_t W, uint32_t H, uint32_t B, bool flat, int E) {
+  DPlan P{};
+  if (flat) {
+    W = W * H;
+    H = 1;
+  }
+  P.width = W;
+  P.height = H;
+  P.batch = B;
+  P.tiles_per_row = (W + uint32_t(E) - 1) / uint32_t(E);
+  const uint64_t tiles = uint64_t(H) * P.tiles_per_row;
+  if (tiles >= (uint64_t(1) << 32) - 256) fail(FK_E_CAPACITY_OVERFLOW, "plane too large for one launch");
+  P.tiles = uint32_t(tiles);
+  P.tpr = make_fastdiv(P.tiles_per_row);
+  return P;
+}
+
+int current_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    fail(FK_E_NO_DEVICE, "no CUDA device visible");
+  }
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  int major = 0;
+  cuda_check(cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev), "cudaDeviceGetAttribute");
+  if (major != 10) fail(FK_E_NO_DEVICE, "libfk_cuda.so is built for sm_100a (B200); device " +
+                                            std::to_string(dev) + " is sm_" + std::to_string(major) + "x");
+  return dev;
+}
+
+std::mutex g_build_mu;
+
+DeviceProgram& ensure_program(const Pipeline& p) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lock(g_build_mu);
+  auto& slot = const_cast<Pipeline&>(p).dev;
+  if (!slot || slot->device != dev) slot = build_program(p, dev);
+  return *slot;
+}
+
+struct Timer {
+  cudaStream_t st;
+  bool on;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Timer(cudaStream_t s, bool enabled) : st(s), on(enabled) {
+    if (!on) return;
+    cuda_check(cudaEventCreate(&a), "cudaEventCreate");
+    cuda_check(cudaEventCreate(&b), "cudaEventCreate");
+    cuda_check(cudaEventRecord(a, st), "cudaEventRecord");
+  }
+  double stop() {
+    if (!on) return 0.0;
+    cuda_check(cudaEventRecord(b, st), "cudaEventRecord");
+    cuda_check(cudaEventSynchronize(b), "cudaEventSynchronize");
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+  }
+  ~Timer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+};
+
+void launch(int cls, const DPlan& P, cudaStream_t st, uint64_t& count) {
+  cuda_check(launch_generic(cls, P, st), "fk_transform_generic launch");
+  ++count;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+}
+
+uint64_t now_ns() {
+  return uint64_t(std::chrono::duration_cast<std::chrono::nanoseconds>(
+                      std::chrono::steady_clock::now().time_since_epoch()).count());
+}
+
+void fill_plan_io(DPlan& P, const DeviceProgram& dp, const Pipeline& p) {
+  P.post = dp.d_post;
+  P.def_kind = dp.def_kind;
+  std::memcpy(P.def, dp.def, sizeof P.def);
+  P.write_kind = uint32_t(p.write.in_kind);
+  const uint32_t wid = p.write.id == FK_OP_BATCH_WRITE ? p.write.w_inner : p.write.id;
+  P.write_mode = wid == FK_OP_SPLIT_WRITE ? WR_SPLIT : WR_DIRECT;
+}
+
+}  // namespace
+
+void check_config(const fk_exec_config* c) {  // executor.cpp:20-25
+  if (!c) return;
+  if (c->chunk_rows < 1) fail(FK_E_INVALID_CONFIG, "chunk_rows must be >= 1");
+  const int b = c->coarsen_block;
+  if (!(b == 1 || b == 2 || b == 4 || b == 8 || b == 16))
+    fail(FK_E_INVALID_CONFIG, "coarsening block must be one of 1/2/4/8/16");
+  if (c->workers < 0) fail(FK_E_INVALID_CONFIG, "workers must be >= 0");
+}
+
+fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
+  check_config(cfg);
+  const uint64_t t0 = now_ns();
+  DeviceProgram& dp = ensure_program(p);
+  cudaStream_t st = cfg ? static_cast<cudaStream_t>(cfg->stream) : nullptr;
+  fk_exec_report r{};
+  Timer timer(st, cfg && (cfg->flags & FK_EXEC_TIMED));
+  const int cls = generic_state_class(dp.fused_wide, dp.fused_lanes);
+  DPlan P = base_plan(p.space.width, p.space.height, p.space.batch, dp.read_flat && dp.write_flat,
+                      generic_elems(cls));
+  fill_plan_io(P, dp, p);
+  P.n_ops = dp.n_fops;
+  P.ops = dp.d_fops;
+  P.reads = dp.d_reads;
+  P.writes = dp.d_writes;
+  launch(cls, P, st, r.kernels_launched);
+  r.device_ms = timer.stop();
+  r.wall_time_ns = now_ns() - t0;
+  const Traffic t = analytic_traffic(p);
+  r.bytes_read = t.fused_read;
+  r.bytes_written = t.fused_written;
+  r.passes = 1;
+  r.points_visited = uint64_t(p.space.width) * p.space.height * p.space.batch;
+  r.path = FK_PATH_GENERIC;
+  return r;
+}
+
+fk_exec_report execute_unfused(const Pipeline& p, const fk_exec_config* cfg) {
+  check_config(cfg);
+  const uint64_t t0 = now_ns();
+  DeviceProgram& dp = ensure_program(p);
+  cudaStream_t st = cfg ? static_cast<cudaStream_t>(cfg->stream) : nullptr;
+  fk_exec_report r{};
+  Timer timer(st, cfg && (cfg->flags & FK_EXEC_TIMED));
+  const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
+  const size_t n = p.compute.size();
+  const Traffic t = analytic_traffic(p);
+  if (n == 0) {  // executor.cpp:144-166: one read -> write sweep
+    const int cls = generic_state_class(dp.fused_wide, dp.fused_lanes);
+    DPlan P = base_plan(W, H, B, dp.read_flat && dp.write_flat, generic_elems(cls));
+    fill_plan_io(P, dp, p);
+    P.reads = dp.d_reads;
+    P.writes = dp.d_writes;
+    launch(cls, P, st, r.kernels_launched);
+  } else {
+    const uint64_t pts = uint64_t(W) * H;
+    void* prev = nullptr;
+    uint32_t prev_kind = 0;
+    for (size_t i = 0; i <= n; ++i) {
+      const bool final_pass = i == n;
+      bool wide = false;
+      int lanes = 1;
+      DSample rd{};
+      if (i == 0) {
+        wide = dp.read_wide;
+        lanes = dp.read_lanes;
+      } else {  // load_block of the previous intermediate (executor.cpp:120-124)
+        add_kind(prev_kind, wide, lanes);
+        rd.src = reinterpret_cast<uint64_t>(prev);
+        rd.pitch = uint64_t(W) * bpe(prev_kind);
+        rd.rect_w = rd.out_w = W;
+        rd.rect_h = rd.out_h = H;
+        rd.kind = prev_kind;
+        rd.mode = RD_DIRECT;
+        rd.flags = SF_LANE_ALIGNED;
+      }
+      void* next = nullptr;
+      uint32_t out_kind = 0;
+      if (!final_pass) {
+        out_kind = uint32_t(p.compute[i].out_kind);
+        add_kind(uint32_t(p.compute[i].in_kind), wide, lanes);
+        add_kind(out_kind, wide, lanes);
+        cuda_check(cudaMallocAsync(&next, pts * B * bpe(out_kind), st), "cudaMallocAsync(intermediate)");
+        r.intermediate_bytes_allocated += pts * B * bpe(out_kind);
+      } else {
+        add_kind(uint32_t(p.write.in_kind), wide, lanes);
+      }
+      const int cls = generic_state_class(wide, lanes);
+      const bool flat = (i == 0 ? dp.read_flat : true) && (final_pass ? dp.write_flat : true);
+      DPlan P = base_plan(W, H, B, flat, generic_elems(cls));
+      fill_plan_io(P, dp, p);
+      if (i == 0) {
+        P.reads = dp.d_reads;
+      } else {
+        P.rd = rd;
+        P.rd_zstride = pts * bpe(prev_kind);
+      }
+      if (final_pass) {  // final sweep through the write op (executor.cpp:197-213)
+        P.writes = dp.d_writes;
+      } else {           // store_block_to the fresh intermediate (executor.cpp:126-130)
+        P.ops = dp.d_ops + i;
+        P.n_ops = 1;
+        P.wr.dst[0] = reinterpret_cast<uint64_t>(next);
+        P.wr.pitch[0] = uint64_t(W) * bpe(out_kind);
+        P.wr.flags = WF_ACTIVE | WF_LANE_ALIGNED;
+        P.wr_zstride = pts * bpe(out_kind);
+        P.write_kind = out_kind;
+        P.write_mode = WR_DIRECT;
+      }
+      launch(cls, P, st, r.kernels_launched);
+      if (prev) cuda_check(cudaFreeAsync(prev, st), "cudaFreeAsync(intermediate)");
+      prev = next;
+      prev_kind = out_kind;
+    }
+  }
+  r.device_ms = timer.stop();
+  r.wall_time_ns = now_ns() - t0;
+  r.bytes_read = t.unfused_read;
+  r.bytes_written = t.unfused_written;
+  r.passes = n + 1;
+  r.points_visited = uint64_t(W) * H * B * r.passes;
+  r.path = FK_PATH_GENERIC;
+  return r;
+}
+
+uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+std::string device_info() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+    cudaGetLastError();
+    return "no CUDA device";
+  }
+  int dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceProp prop{};
+  cudaGetDeviceProperties(&prop, dev);
+  return std::string(prop.name) + " sm_" + std::to_string(prop.major) + std::to_string(prop.minor) + " SMs=" +
+         std::to_string(prop.multiProcessorCount) + " L2=" + std::to_string(prop.l2CacheSize);
+}
+
+}  // namespace fk

@@ -1,0 +1,65 @@
+// fk_generic.cu — the interpreted-chain fused kernel (TransformDPP).
+//
+// One launch runs Read -> Compute* -> Write for every point of the iteration
+// space: blockIdx.z is the batch plane z (horizontal fusion),
+// each thread owns E consecutive x of one row (thread coarsening) and keeps all
+// intermediates in registers (vertical fusion). The compute chain is a device
+// program walked with warp-uniform dispatch, so ANY validated chain runs fused
+// in one kernel; chains the registry knows run the compiled kernels instead
+// (fk_compiled.cu). Four instantiations cover every chain: 32/64-bit lanes x 1/3 lanes.
+#include <cuda_runtime.h>
+
+#include "fk_launch.hpp"
+#include "fk_stages.cuh"
+
+namespace fk {
+
+template <class Lane, int L, int E>
+__global__ void __launch_bounds__(256) fk_transform_generic(const __grid_constant__ DPlan P) {
+  const uint32_t t = blockIdx.x * 256u + threadIdx.x;
+  if (t >= P.tiles) return;
+  const uint32_t y = dev::fastdiv(t, P.tpr);
+  const uint32_t x = (t - y * P.tiles_per_row) * E;
+  const int n = (P.width - x) < uint32_t(E) ? int(P.width - x) : E;
+  for (uint32_t z = blockIdx.z; z < P.batch; z += gridDim.z) {
+    DSample s;
+    if (P.reads) {
+      s = P.reads[z];
+    } else {
+      s = P.rd;
+      s.src += uint64_t(z) * P.rd_zstride;
+    }
+    DWrite w;
+    if (P.writes) {
+      w = P.writes[z];
+    } else {
+      w = P.wr;
+      w.dst[0] += uint64_t(z) * P.wr_zstride;
+    }
+    Lane v[E][L];
+    dev::read_tile(P, s, z, x, y, n, v);
+    for (uint32_t i = 0; i < P.n_ops; ++i) {
+      const DOp op = P.ops[i];
+      dev::apply_op(op, z, v);
+    }
+    dev::write_tile(P, w, x, y, n, v);
+  }
+}
+
+int generic_state_class(bool wide, int lanes) { return (wide ? 2 : 0) + (lanes == 3 ? 1 : 0); }
+
+int generic_elems(int cls) { return cls == 0 ? 8 : 4; }
+
+cudaError_t launch_generic(int cls, const DPlan& P, cudaStream_t st) {
+  if (P.tiles == 0 || P.batch == 0) return cudaSuccess;
+  const dim3 grid((P.tiles + 255u) / 256u, 1, P.batch < 65535u ? P.batch : 65535u);
+  switch (cls) {
+    case 0: fk_transform_generic<uint32_t, 1, 8><<<grid, 256, 0, st>>>(P); break;
+    case 1: fk_transform_generic<uint32_t, 3, 4><<<grid, 256, 0, st>>>(P); break;
+    case 2: fk_transform_generic<uint64_t, 1, 4><<<grid, 256, 0, st>>>(P); break;
+    default: fk_transform_generic<uint64_t, 3, 4><<<grid, 256, 0, st>>>(P); break;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace fk

@@ -1,0 +1,15 @@
+// fk_launch.hpp — host entry points of the kernel families.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "fk_devprog.hpp"
+
+namespace fk {
+
+// interpreted-chain kernel (fk_generic.cu)
+int generic_state_class(bool wide, int lanes);  // 0..3
+int generic_elems(int cls);                     // E: consecutive x per thread
+cudaError_t launch_generic(int cls, const DPlan& P, cudaStream_t st);
+
+}  // namespace fk
