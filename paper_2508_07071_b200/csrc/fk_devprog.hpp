@@ -58,11 +58,22 @@ struct FastDiv {             // n / d for 32-bit n (Granlund-Montgomery round-up
   uint32_t d, m, s;
 };
 
+// Per-CTA resample tables in shared memory: the sampling coordinates depend only
+// on the output column (x) or row (y), so center_coord/floor/clamp (ops.cpp:253-270)
+// run once per column and row of the CTA instead of once per pixel.
+struct XEnt { uint32_t o0, o1; double f; };  // tap byte offsets in the row (x0 + clamp) * bpe, fx
+struct YEnt { uint64_t r0, r1; double f; };  // tap row byte offsets (y0 + clamp) * pitch, fy
+constexpr uint32_t kBlock = 256;             // threads per CTA
+constexpr uint32_t kXCap = 1024;             // table path when out_w <= kXCap
+constexpr uint32_t kYCap = 160;              // rows one CTA may span (host keeps tiles_per_cta within it)
+
 struct DPlan {
   uint32_t width, height, batch;  // iteration space (flattened to height 1 when contiguous)
   uint32_t tiles_per_row;
   FastDiv tpr;
   uint32_t tiles;            // tiles per plane = height * tiles_per_row
+  uint32_t tiles_per_cta;    // contiguous tile range one CTA walks (multiple of the block size)
+  uint32_t pad0;
   uint32_t n_ops;
   const DOp* ops;            // compute program
   const DOp* post;           // folded-unary programs referenced by DSample::post_off

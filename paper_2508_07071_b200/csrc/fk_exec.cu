@@ -229,6 +229,7 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
     }
     s.src = reinterpret_cast<uint64_t>(sp->source.data);
     s.pitch = pitch_of(sp->source);
+    if (s.pitch >= (uint64_t(1) << 32)) fail(FK_E_CAPACITY_OVERFLOW, "source rows above 4 GiB");
     s.x0 = sp->x0;
     s.y0 = sp->y0;
     s.rect_w = sp->rect_w;
@@ -306,9 +307,20 @@ DPlan base_plan(uint32_t W, uint32_t H, uint32_t B, bool flat, int E) {
   P.batch = B;
   P.tiles_per_row = (W + uint32_t(E) - 1) / uint32_t(E);
   const uint64_t tiles = uint64_t(H) * P.tiles_per_row;
-  if (tiles >= (uint64_t(1) << 32) - 256) fail(FK_E_CAPACITY_OVERFLOW, "plane too large for one launch");
+  if (tiles >= (uint64_t(1) << 32) - 65536) fail(FK_E_CAPACITY_OVERFLOW, "plane too large for one launch");
   P.tiles = uint32_t(tiles);
   P.tpr = make_fastdiv(P.tiles_per_row);
+  // Each CTA walks a contiguous tile range: up to 16 tiles per thread, enough
+  // CTAs to fill 148 SMs several times over, and few enough rows per CTA that
+  // the resample y-table fits (kYCap).
+  const uint64_t planes = B;
+  uint32_t per_thread = 16;
+  while (per_thread > 1 && planes * ((tiles + uint64_t(kBlock) * per_thread - 1) / (uint64_t(kBlock) * per_thread)) < 148u * 8u)
+    per_thread /= 2;
+  uint64_t tpc = uint64_t(kBlock) * per_thread;
+  const uint64_t max_rows_tiles = uint64_t(kYCap - 2) * P.tiles_per_row;
+  while (tpc > kBlock && tpc > max_rows_tiles) tpc -= kBlock;
+  P.tiles_per_cta = uint32_t(tpc);
   return P;
 }
 

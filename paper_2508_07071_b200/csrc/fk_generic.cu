@@ -15,12 +15,15 @@
 namespace fk {
 
 template <class Lane, int L, int E>
-__global__ void __launch_bounds__(256) fk_transform_generic(const __grid_constant__ DPlan P) {
-  const uint32_t t = blockIdx.x * 256u + threadIdx.x;
-  if (t >= P.tiles) return;
-  const uint32_t y = dev::fastdiv(t, P.tpr);
-  const uint32_t x = (t - y * P.tiles_per_row) * E;
-  const int n = (P.width - x) < uint32_t(E) ? int(P.width - x) : E;
+__global__ void __launch_bounds__(kBlock) fk_transform_generic(const __grid_constant__ DPlan P) {
+  __shared__ XEnt xt[kXCap];
+  __shared__ YEnt yt[kYCap];
+  // this CTA walks tiles [t_begin, t_end) of plane z; a tile is E consecutive x of one row
+  const uint32_t t_begin = blockIdx.x * P.tiles_per_cta;
+  if (t_begin >= P.tiles) return;
+  const uint32_t t_end = min(t_begin + P.tiles_per_cta, P.tiles);
+  const uint32_t y_first = dev::fastdiv(t_begin, P.tpr);
+  const uint32_t rows = dev::fastdiv(t_end - 1, P.tpr) - y_first + 1;
   for (uint32_t z = blockIdx.z; z < P.batch; z += gridDim.z) {
     DSample s;
     if (P.reads) {
@@ -36,13 +39,25 @@ __global__ void __launch_bounds__(256) fk_transform_generic(const __grid_constan
       w = P.wr;
       w.dst[0] += uint64_t(z) * P.wr_zstride;
     }
-    Lane v[E][L];
-    dev::read_tile(P, s, z, x, y, n, v);
-    for (uint32_t i = 0; i < P.n_ops; ++i) {
-      const DOp op = P.ops[i];
-      dev::apply_op(op, z, v);
+    // resampling planes: per-column / per-row coordinates once per CTA (uniform branch)
+    const bool tab = s.mode != RD_DIRECT && !(s.flags & SF_DEFAULT) && P.width <= kXCap && rows <= kYCap;
+    if (tab) {
+      __syncthreads();
+      dev::build_tables(s, P.width, y_first, rows, xt, yt);
+      __syncthreads();
     }
-    dev::write_tile(P, w, x, y, n, v);
+    for (uint32_t t = t_begin + threadIdx.x; t < t_end; t += kBlock) {
+      const uint32_t y = dev::fastdiv(t, P.tpr);
+      const uint32_t x = (t - y * P.tiles_per_row) * E;
+      const int n = (P.width - x) < uint32_t(E) ? int(P.width - x) : E;
+      Lane v[E][L];
+      dev::read_tile(P, s, z, x, y, n, v, tab ? xt : nullptr, tab ? yt + (y - y_first) : nullptr);
+      for (uint32_t i = 0; i < P.n_ops; ++i) {
+        const DOp op = P.ops[i];
+        dev::apply_op(op, z, v);
+      }
+      dev::write_tile(P, w, x, y, n, v);
+    }
   }
 }
 
@@ -52,12 +67,12 @@ int generic_elems(int cls) { return cls == 0 ? 8 : 4; }
 
 cudaError_t launch_generic(int cls, const DPlan& P, cudaStream_t st) {
   if (P.tiles == 0 || P.batch == 0) return cudaSuccess;
-  const dim3 grid((P.tiles + 255u) / 256u, 1, P.batch < 65535u ? P.batch : 65535u);
+  const dim3 grid((P.tiles + P.tiles_per_cta - 1) / P.tiles_per_cta, 1, P.batch < 65535u ? P.batch : 65535u);
   switch (cls) {
-    case 0: fk_transform_generic<uint32_t, 1, 8><<<grid, 256, 0, st>>>(P); break;
-    case 1: fk_transform_generic<uint32_t, 3, 4><<<grid, 256, 0, st>>>(P); break;
-    case 2: fk_transform_generic<uint64_t, 1, 4><<<grid, 256, 0, st>>>(P); break;
-    default: fk_transform_generic<uint64_t, 3, 4><<<grid, 256, 0, st>>>(P); break;
+    case 0: fk_transform_generic<uint32_t, 1, 8><<<grid, kBlock, 0, st>>>(P); break;
+    case 1: fk_transform_generic<uint32_t, 3, 4><<<grid, kBlock, 0, st>>>(P); break;
+    case 2: fk_transform_generic<uint64_t, 1, 4><<<grid, kBlock, 0, st>>>(P); break;
+    default: fk_transform_generic<uint64_t, 3, 4><<<grid, kBlock, 0, st>>>(P); break;
   }
   return cudaGetLastError();
 }

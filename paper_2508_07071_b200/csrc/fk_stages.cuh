@@ -180,8 +180,122 @@ __device__ __forceinline__ void load_elem(const uint8_t* p, bool al, Lane (&v)[E
   for (int l = 0; l < T::nl; ++l) v[e][l] = load_lane<T::lk, Lane>(p + l * T::lb, al);
 }
 
+// Two horizontally adjacent u8x3 taps (6 bytes at p) through two aligned 32-bit loads:
+// the 8-byte window [p & ~3, +8) always holds them and never leaves the words that
+// contain in-bounds bytes, so it cannot fault past an allocation.
+__device__ __forceinline__ uint64_t load_u8x3_pair(const uint8_t* p) {
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+  const uint64_t v = uint64_t(__ldg(w)) | (uint64_t(__ldg(w + 1)) << 32);
+  return v >> ((a & 3) * 8);
+}
+
+// bilinear_sample, ops.cpp:259-299, for one output pixel whose taps are at byte
+// offsets o0/o1 of rows r0/r1. u8 lanes take an exact shortcut for int->double
+// (2^52 + v is a double whose low word is v) and for nearbyint (adding 1.5*2^52
+// rounds to an integer ties-to-even in the low word); the lerp arithmetic is the
+// reference's, op for op, in double.
 template <uint32_t K, class Lane, int L, int E>
-__device__ __forceinline__ void read_kind(const DSample& s, uint32_t x, uint32_t y, int n, Lane (&v)[E][L]) {
+__device__ __forceinline__ void bilinear_px(const uint8_t* r0, const uint8_t* r1, uint32_t o0, uint32_t o1,
+                                            double fx, double fy, bool al, Lane (&v)[E][L], int e) {
+  using T = KindT<K>;
+  if constexpr (T::lk == FK_U8) {
+    uint32_t ta[T::nl], tb[T::nl], tc[T::nl], td[T::nl];
+    if (T::nl == 3 && o1 == o0 + 3) {
+      const uint64_t top = load_u8x3_pair(r0 + o0), bot = load_u8x3_pair(r1 + o0);
+#pragma unroll
+      for (int l = 0; l < T::nl; ++l) {
+        ta[l] = uint32_t(top >> (8 * l)) & 0xffu;
+        tb[l] = uint32_t(top >> (8 * l + 24)) & 0xffu;
+        tc[l] = uint32_t(bot >> (8 * l)) & 0xffu;
+        td[l] = uint32_t(bot >> (8 * l + 24)) & 0xffu;
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < T::nl; ++l) {
+        ta[l] = __ldg(r0 + o0 + l);
+        tb[l] = __ldg(r0 + o1 + l);
+        tc[l] = __ldg(r1 + o0 + l);
+        td[l] = __ldg(r1 + o1 + l);
+      }
+    }
+    constexpr double kTwo52 = 4503599627370496.0;        // 2^52
+    constexpr double kRound = 6755399441055744.0;        // 1.5 * 2^52
+#pragma unroll
+    for (int l = 0; l < T::nl; ++l) {
+      const double A = __hiloint2double(0x43300000, int(ta[l]));   // 2^52 + a, exact
+      const double B = __hiloint2double(0x43300000, int(tb[l]));
+      const double C = __hiloint2double(0x43300000, int(tc[l]));
+      const double D = __hiloint2double(0x43300000, int(td[l]));
+      const double a = __dsub_rn(A, kTwo52), c = __dsub_rn(C, kTwo52);         // exact
+      const double top = __dadd_rn(a, __dmul_rn(__dsub_rn(B, A), fx));          // a + (b - a) * fx
+      const double bot = __dadd_rn(c, __dmul_rn(__dsub_rn(D, C), fx));          // c + (d - c) * fx
+      const double res = __dadd_rn(top, __dmul_rn(__dsub_rn(bot, top), fy));   // top + (bot - top) * fy
+      // res is in [0, 255] (a lerp of values in [0, 255] with t in [0, 1) under RN), so
+      // round_clamp_u8 reduces to nearbyint, i.e. the low word of res + 1.5 * 2^52.
+      v[e][l] = Lane(uint32_t(__double2loint(__dadd_rn(res, kRound))));
+    }
+  } else {
+#pragma unroll
+    for (int l = 0; l < T::nl; ++l) {
+      const int lo = l * T::lb;
+      const double a = lane_to_double<T::lk>(load_lane<T::lk, Lane>(r0 + o0 + lo, al));
+      const double b = lane_to_double<T::lk>(load_lane<T::lk, Lane>(r0 + o1 + lo, al));
+      const double c = lane_to_double<T::lk>(load_lane<T::lk, Lane>(r1 + o0 + lo, al));
+      const double d = lane_to_double<T::lk>(load_lane<T::lk, Lane>(r1 + o1 + lo, al));
+      v[e][l] = lane_from_double<T::lk, Lane>(lerp(lerp(a, b, fx), lerp(c, d, fx), fy));
+    }
+  }
+}
+
+// Sampling coordinates of output column i (ops.cpp:259-270 / 301-306) for a table entry.
+__device__ __forceinline__ XEnt x_entry(const DSample& s, uint32_t i, uint32_t bpe) {
+  XEnt x;
+  const long long maxx = (long long)s.rect_w - 1;
+  if (s.mode == RD_BILINEAR) {
+    const double cx = center_coord(i, s.rect_w, s.out_w);
+    const double fl = floor(cx);
+    const long long ix = (long long)fl;
+    x.o0 = uint32_t((s.x0 + clamp_ll(ix, 0, maxx)) * bpe);
+    x.o1 = uint32_t((s.x0 + clamp_ll(ix + 1, 0, maxx)) * bpe);
+    x.f = __dsub_rn(cx, fl);
+  } else {
+    const double cx = __ddiv_rn(__dmul_rn(__dadd_rn((double)i, 0.5), (double)s.rect_w), (double)s.out_w);
+    x.o0 = x.o1 = uint32_t((s.x0 + clamp_ll((long long)floor(cx), 0, maxx)) * bpe);
+    x.f = 0.0;
+  }
+  return x;
+}
+__device__ __forceinline__ YEnt y_entry(const DSample& s, uint32_t j) {
+  YEnt y;
+  const long long maxy = (long long)s.rect_h - 1;
+  if (s.mode == RD_BILINEAR) {
+    const double cy = center_coord(j, s.rect_h, s.out_h);
+    const double fl = floor(cy);
+    const long long iy = (long long)fl;
+    y.r0 = uint64_t(s.y0 + clamp_ll(iy, 0, maxy)) * s.pitch;
+    y.r1 = uint64_t(s.y0 + clamp_ll(iy + 1, 0, maxy)) * s.pitch;
+    y.f = __dsub_rn(cy, fl);
+  } else {
+    const double cy = __ddiv_rn(__dmul_rn(__dadd_rn((double)j, 0.5), (double)s.rect_h), (double)s.out_h);
+    y.r0 = y.r1 = uint64_t(s.y0 + clamp_ll((long long)floor(cy), 0, maxy)) * s.pitch;
+    y.f = 0.0;
+  }
+  return y;
+}
+
+// Resample tables for this CTA's rows [y_first, y_first + rows) (block-cooperative).
+__device__ __forceinline__ void build_tables(const DSample& s, uint32_t width, uint32_t y_first, uint32_t rows,
+                                             XEnt* xt, YEnt* yt) {
+  constexpr uint32_t kBpe[6] = {1, 4, 8, 3, 12, 24};
+  const uint32_t b = kBpe[s.kind];
+  for (uint32_t i = threadIdx.x; i < width; i += blockDim.x) xt[i] = x_entry(s, i, b);
+  for (uint32_t j = threadIdx.x; j < rows; j += blockDim.x) yt[j] = y_entry(s, y_first + j);
+}
+
+template <uint32_t K, class Lane, int L, int E>
+__device__ __forceinline__ void read_kind(const DSample& s, uint32_t x, uint32_t y, int n, Lane (&v)[E][L],
+                                          const XEnt* xt, const YEnt* yt) {
   if constexpr (fits<K, Lane, L>()) {
     using T = KindT<K>;
     const bool al = (s.flags & SF_LANE_ALIGNED) != 0;
@@ -200,47 +314,18 @@ __device__ __forceinline__ void read_kind(const DSample& s, uint32_t x, uint32_t
 #pragma unroll
       for (int e = 0; e < E; ++e)
         if (e < n) load_elem<K>(p + e * T::bpe, al, v, e);
-    } else if (s.mode == RD_NEAREST) {  // nearest_sample, ops.cpp:301-310
-      const double cy = __ddiv_rn(__dmul_rn(__dadd_rn((double)y, 0.5), (double)s.rect_h), (double)s.out_h);
-      const long long sy = s.y0 + clamp_ll((long long)floor(cy), 0, (long long)s.rect_h - 1);
-      const uint8_t* row = base + uint64_t(sy) * s.pitch;
+      return;
+    }
+    // resampling read: coordinates from the CTA tables when present, else computed here
+    const YEnt ye = yt ? *yt : y_entry(s, y);
+    const uint8_t* r0 = base + ye.r0;
+    const uint8_t* r1 = base + ye.r1;
 #pragma unroll
-      for (int e = 0; e < E; ++e) {
-        if (e < n) {
-          const double cx = __ddiv_rn(__dmul_rn(__dadd_rn((double)(x + e), 0.5), (double)s.rect_w), (double)s.out_w);
-          const long long sx = s.x0 + clamp_ll((long long)floor(cx), 0, (long long)s.rect_w - 1);
-          load_elem<K>(row + uint64_t(sx) * T::bpe, al, v, e);
-        }
-      }
-    } else {  // bilinear_sample, ops.cpp:259-299
-      const double cy = center_coord(y, s.rect_h, s.out_h);
-      const double fiy = floor(cy);
-      const long long iy = (long long)fiy;
-      const double fy = __dsub_rn(cy, fiy);
-      const long long maxy = (long long)s.rect_h - 1, maxx = (long long)s.rect_w - 1;
-      const uint8_t* r0 = base + uint64_t(s.y0 + clamp_ll(iy, 0, maxy)) * s.pitch;
-      const uint8_t* r1 = base + uint64_t(s.y0 + clamp_ll(iy + 1, 0, maxy)) * s.pitch;
-#pragma unroll
-      for (int e = 0; e < E; ++e) {
-        if (e < n) {
-          const double cx = center_coord(x + e, s.rect_w, s.out_w);
-          const double fix = floor(cx);
-          const long long ix = (long long)fix;
-          const double fx = __dsub_rn(cx, fix);
-          const uint64_t o0 = uint64_t(s.x0 + clamp_ll(ix, 0, maxx)) * T::bpe;
-          const uint64_t o1 = uint64_t(s.x0 + clamp_ll(ix + 1, 0, maxx)) * T::bpe;
-#pragma unroll
-          for (int l = 0; l < T::nl; ++l) {
-            const int lo = l * T::lb;
-            const double a = lane_to_double<T::lk>(load_lane<T::lk, Lane>(r0 + o0 + lo, al));
-            const double b = lane_to_double<T::lk>(load_lane<T::lk, Lane>(r0 + o1 + lo, al));
-            const double c = lane_to_double<T::lk>(load_lane<T::lk, Lane>(r1 + o0 + lo, al));
-            const double d = lane_to_double<T::lk>(load_lane<T::lk, Lane>(r1 + o1 + lo, al));
-            const double top = lerp(a, b, fx);
-            const double bot = lerp(c, d, fx);
-            v[e][l] = lane_from_double<T::lk, Lane>(lerp(top, bot, fy));
-          }
-        }
+    for (int e = 0; e < E; ++e) {
+      if (e < n) {
+        const XEnt xe = xt ? xt[x + e] : x_entry(s, x + e, T::bpe);
+        if (s.mode == RD_NEAREST) load_elem<K>(r0 + xe.o0, al, v, e);  // nearest_sample, ops.cpp:301-310
+        else bilinear_px<K>(r0, r1, xe.o0, xe.o1, xe.f, ye.f, al, v, e);
       }
     }
   }
@@ -249,7 +334,7 @@ __device__ __forceinline__ void read_kind(const DSample& s, uint32_t x, uint32_t
 // read_exec_block, ops.cpp:361-381, plus the folded unaries (sample_block :343)
 template <class Lane, int L, int E>
 __device__ __forceinline__ void read_tile(const DPlan& P, const DSample& s, uint32_t z, uint32_t x, uint32_t y,
-                                          int n, Lane (&v)[E][L]) {
+                                          int n, Lane (&v)[E][L], const XEnt* xt, const YEnt* yt) {
   if (s.flags & SF_DEFAULT) {  // z >= active_count: default value, no post ops
 #pragma unroll
     for (int e = 0; e < E; ++e)
@@ -258,12 +343,12 @@ __device__ __forceinline__ void read_tile(const DPlan& P, const DSample& s, uint
     return;
   }
   switch (s.kind) {
-    case FK_U8: read_kind<FK_U8>(s, x, y, n, v); break;
-    case FK_F32: read_kind<FK_F32>(s, x, y, n, v); break;
-    case FK_F64: read_kind<FK_F64>(s, x, y, n, v); break;
-    case FK_U8X3: read_kind<FK_U8X3>(s, x, y, n, v); break;
-    case FK_F32X3: read_kind<FK_F32X3>(s, x, y, n, v); break;
-    default: read_kind<FK_F64X3>(s, x, y, n, v); break;
+    case FK_U8: read_kind<FK_U8>(s, x, y, n, v, xt, yt); break;
+    case FK_F32: read_kind<FK_F32>(s, x, y, n, v, xt, yt); break;
+    case FK_F64: read_kind<FK_F64>(s, x, y, n, v, xt, yt); break;
+    case FK_U8X3: read_kind<FK_U8X3>(s, x, y, n, v, xt, yt); break;
+    case FK_F32X3: read_kind<FK_F32X3>(s, x, y, n, v, xt, yt); break;
+    default: read_kind<FK_F64X3>(s, x, y, n, v, xt, yt); break;
   }
   for (uint32_t i = 0; i < s.post_len; ++i) {
     const DOp op = P.post[s.post_off + i];
