@@ -99,6 +99,7 @@ typedef struct fk_exec_config {
 #define FK_EXEC_TIMED 0x1u         /* CUDA: bracket the launch(es) with events and synchronise: fills device_ms */
 #define FK_EXEC_FORCE_GENERIC 0x2u /* CUDA: use the interpreted-chain kernel even when a compiled chain matches */
 #define FK_EXEC_SERIAL 0x4u        /* CPU backends: execute_fused_serial (executor.hpp:42-45) */
+#define FK_EXEC_NO_LUT 0x8u        /* CUDA: never tabulate u8 lane-wise chains (measure the op-by-op path) */
 
 /* ExecReport, executor.hpp:27-34, plus device-side fields. */
 typedef struct fk_exec_report {

@@ -47,6 +47,7 @@ SWAP_RB, TO_GRAY_F32 = 0, 1
 EXEC_TIMED = 0x1
 EXEC_FORCE_GENERIC = 0x2
 EXEC_SERIAL = 0x4
+EXEC_NO_LUT = 0x8
 
 PATH_CPU, PATH_GENERIC, PATH_COMPILED = 0, 1, 2
 

@@ -12,8 +12,10 @@ namespace fk {
 
 // read modes, resolved on the host from SampleReadParams::resizing()/mode (ops.cpp:327-344)
 enum : uint32_t { RD_DIRECT = 0, RD_NEAREST = 1, RD_BILINEAR = 2 };
-// DSample::flags
-enum : uint32_t { SF_DEFAULT = 1u, SF_LANE_ALIGNED = 2u };
+// DSample::flags. SF_LUT_SRC: u8 lanes and a lane-wise folded-unary program, so
+// post+compute can be tabulated over the 256 possible lane values.
+// SF_POST_SWAP: the folded unaries swap lanes 0/2 an odd number of times.
+enum : uint32_t { SF_DEFAULT = 1u, SF_LANE_ALIGNED = 2u, SF_LUT_SRC = 4u, SF_POST_SWAP = 8u };
 // DWrite::flags
 enum : uint32_t { WF_ACTIVE = 1u, WF_LANE_ALIGNED = 2u, WF_STREAM = 4u };
 // write modes
@@ -30,7 +32,7 @@ struct DSample {             // one plane's read (SampleReadParams, ops.hpp:78-9
   uint32_t out_w, out_h;
   uint32_t kind;             // source ScalarKind
   uint32_t mode;             // RD_*
-  uint32_t post_off, post_len;  // folded unaries (index into DPlan::post)
+  uint32_t post_off, post_len;  // folded unaries: absolute index into the DPlan program table
   uint32_t flags;            // SF_*
   uint32_t pad;
 };
@@ -67,16 +69,20 @@ constexpr uint32_t kBlock = 256;             // threads per CTA
 constexpr uint32_t kXCap = 1024;             // table path when out_w <= kXCap
 constexpr uint32_t kYCap = 160;              // rows one CTA may span (host keeps tiles_per_cta within it)
 
+constexpr uint32_t kProg = 24;  // ops carried in kernel-parameter space (constant bank)
+
 struct DPlan {
   uint32_t width, height, batch;  // iteration space (flattened to height 1 when contiguous)
   uint32_t tiles_per_row;
   FastDiv tpr;
   uint32_t tiles;            // tiles per plane = height * tiles_per_row
   uint32_t tiles_per_cta;    // contiguous tile range one CTA walks (multiple of the block size)
-  uint32_t pad0;
-  uint32_t n_ops;
-  const DOp* ops;            // compute program
-  const DOp* post;           // folded-unary programs referenced by DSample::post_off
+  uint32_t n_ops;            // compute program length
+  uint32_t prog_inline;      // 1: program table is prog[] below (kernel params), else `table`
+  uint32_t lut_ok;           // compute program is lane-wise (LUT-able for u8 sources)
+  uint32_t prog_swap;        // compute program swaps lanes 0/2 an odd number of times
+  const DOp* table;          // [compute ops..., folded-unary programs...] in HBM (long programs)
+  DOp prog[kProg];           // same layout, inline
   const DSample* reads;      // batch entries; nullptr -> affine read below
   const DWrite* writes;      // batch entries; nullptr -> affine write below
   DSample rd;                // affine read: plane z at rd.src + z * rd_zstride
@@ -85,7 +91,7 @@ struct DPlan {
   uint32_t write_kind;       // element kind reaching the write op
   uint32_t write_mode;       // WR_*
   uint32_t def_kind;         // kind of the BatchRead default value
-  uint32_t pad;
+  uint32_t op_base;          // compute ops are table[op_base, op_base + n_ops); post ops at DSample::post_off
   uint64_t def[3];           // BatchRead default Element (ops.hpp:111), lane-encoded
 };
 

@@ -156,11 +156,12 @@ void add_kind(uint32_t k, bool& wide, int& lanes) {
 
 struct DeviceProgram {
   int device = -1;
-  std::vector<DOp> ops;          // 1:1 with Pipeline::compute (unfused pass i runs ops[i])
-  DOp* d_ops = nullptr;
-  DOp* d_fops = nullptr;         // fused (compressed) program
-  uint32_t n_fops = 0;
-  DOp* d_post = nullptr;
+  // program table: [fused (compressed) ops | 1:1 ops (unfused pass i) | folded-unary programs]
+  std::vector<DOp> table;
+  DOp* d_table = nullptr;
+  uint32_t n_fused = 0, n_ops = 0;
+  bool fused_lut_ok = true;      // every fused op is lane-wise
+  bool fused_swap = false;       // odd number of lane swaps in the fused program
   DSample* d_reads = nullptr;
   DWrite* d_writes = nullptr;
   std::vector<void*> extra;      // BatchArith constant tables
@@ -172,10 +173,10 @@ struct DeviceProgram {
   int read_lanes = 1;
   uint64_t def[3] = {0, 0, 0};
   uint32_t def_kind = 0;
+  Traffic traffic;               // analytic ExecReport counters (computed once)
 
   ~DeviceProgram() {
-    for (void* p : {static_cast<void*>(d_ops), static_cast<void*>(d_fops), static_cast<void*>(d_post),
-                    static_cast<void*>(d_reads), static_cast<void*>(d_writes)})
+    for (void* p : {static_cast<void*>(d_table), static_cast<void*>(d_reads), static_cast<void*>(d_writes)})
       if (p) cudaFree(p);
     for (void* p : extra) cudaFree(p);
   }
@@ -185,12 +186,16 @@ Pipeline::~Pipeline() = default;
 
 namespace {
 
+bool lane_wise(const DOp& d) { return d.cls != OC_GRAY; }
+bool odd_swap(const DOp& d) { return d.cls == OC_SWAP && (d.repeat & 1u); }
+
 std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
   auto dp = std::make_shared<DeviceProgram>();
   dp->device = device;
   const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
 
   // compute program (1:1) + BatchArith constant tables
+  std::vector<DOp> ops;
   for (const Op& op : p.compute) {
     DOp d = encode_compute(op);
     if (op.id == FK_OP_BATCH_ARITH) {
@@ -205,15 +210,22 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
       d.per_z = reinterpret_cast<uint64_t>(t);
       d.per_z_n = uint32_t(op.values.size());
     }
-    dp->ops.push_back(d);
+    ops.push_back(d);
     add_kind(uint32_t(op.in_kind), dp->fused_wide, dp->fused_lanes);
     add_kind(uint32_t(op.out_kind), dp->fused_wide, dp->fused_lanes);
   }
-  const std::vector<DOp> fops = compress(dp->ops);
-  dp->n_fops = uint32_t(fops.size());
+  const std::vector<DOp> fops = compress(ops);
+  dp->n_fused = uint32_t(fops.size());
+  dp->n_ops = uint32_t(ops.size());
+  for (const DOp& d : fops) {
+    dp->fused_lut_ok = dp->fused_lut_ok && lane_wise(d);
+    dp->fused_swap ^= odd_swap(d);
+  }
+  dp->table = fops;
+  dp->table.insert(dp->table.end(), ops.begin(), ops.end());
+  const uint32_t post_base = uint32_t(dp->table.size());
 
   // per-plane reads (BatchRead array, ops.cpp:369-378) + deduplicated post programs
-  std::vector<DOp> post;
   std::map<std::vector<uint32_t>, uint32_t> post_index;
   bool flat = uint64_t(W) * H < (uint64_t(1) << 32);
   dp->def_kind = uint32_t(p.read.out_kind);
@@ -240,22 +252,30 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
     s.mode = !sp->resizing() ? RD_DIRECT : (sp->mode == FK_NEAREST ? RD_NEAREST : RD_BILINEAR);
     s.flags = lane_aligned(sp->source) ? SF_LANE_ALIGNED : 0;
     add_kind(s.kind, dp->read_wide, dp->read_lanes);
+    bool post_lane_wise = true, post_swap = false;
     if (!sp->post.empty()) {
       std::vector<uint32_t> key;
       for (const Folded& f : sp->post) {
         key.insert(key.end(), {f.id, f.in, f.out});
         add_kind(f.in, dp->read_wide, dp->read_lanes);
         add_kind(f.out, dp->read_wide, dp->read_lanes);
+        const DOp d = encode_unary(f);
+        post_lane_wise = post_lane_wise && lane_wise(d);
+        post_swap ^= odd_swap(d);
       }
       auto it = post_index.find(key);
       if (it == post_index.end()) {
-        const uint32_t off = uint32_t(post.size());
-        for (const Folded& f : sp->post) post.push_back(encode_unary(f));
+        const uint32_t off = uint32_t(dp->table.size());
+        for (const Folded& f : sp->post) dp->table.push_back(encode_unary(f));
         it = post_index.emplace(key, off).first;
       }
       s.post_off = it->second;
       s.post_len = uint32_t(sp->post.size());
+    } else {
+      s.post_off = post_base;
     }
+    if (lane_kind(s.kind) == FK_U8 && post_lane_wise) s.flags |= SF_LUT_SRC;
+    if (post_swap) s.flags |= SF_POST_SWAP;
     // contiguous identity read of whole rows -> the plane is one flat run
     flat = flat && s.mode == RD_DIRECT && s.x0 == 0 && s.y0 == 0 && sp->source.row_stride == W;
     dp->reads.push_back(s);
@@ -288,9 +308,8 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
   if (dp->read_wide) dp->fused_wide = true;
   if (dp->read_lanes == 3) dp->fused_lanes = 3;
 
-  dp->d_ops = upload(dp->ops);
-  dp->d_fops = upload(fops);
-  dp->d_post = upload(post);
+  dp->traffic = analytic_traffic(p);
+  dp->d_table = upload(dp->table);
   dp->d_reads = upload(dp->reads);
   dp->d_writes = upload(writes);
   return dp;
@@ -384,14 +403,20 @@ uint64_t now_ns() {
                       std::chrono::steady_clock::now().time_since_epoch()).count());
 }
 
-void fill_plan_io(DPlan& P, const DeviceProgram& dp, const Pipeline& p) {
-  P.post = dp.d_post;
+void fill_plan_io(DPlan& P, const DeviceProgram& dp, const Pipeline& p, const fk_exec_config* cfg) {
+  P.table = dp.d_table;
+  P.prog_inline = dp.table.size() <= kProg ? 1u : 0u;
+  if (P.prog_inline) std::memcpy(P.prog, dp.table.data(), dp.table.size() * sizeof(DOp));
   P.def_kind = dp.def_kind;
   std::memcpy(P.def, dp.def, sizeof P.def);
   P.write_kind = uint32_t(p.write.in_kind);
   const uint32_t wid = p.write.id == FK_OP_BATCH_WRITE ? p.write.w_inner : p.write.id;
   P.write_mode = wid == FK_OP_SPLIT_WRITE ? WR_SPLIT : WR_DIRECT;
+  P.lut_ok = 0;
+  (void)cfg;
 }
+
+bool lut_allowed(const fk_exec_config* cfg) { return !(cfg && (cfg->flags & FK_EXEC_NO_LUT)); }
 
 }  // namespace
 
@@ -414,17 +439,18 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
   const int cls = generic_state_class(dp.fused_wide, dp.fused_lanes);
   DPlan P = base_plan(p.space.width, p.space.height, p.space.batch, dp.read_flat && dp.write_flat,
                       generic_elems(cls));
-  fill_plan_io(P, dp, p);
-  P.n_ops = dp.n_fops;
-  P.ops = dp.d_fops;
+  fill_plan_io(P, dp, p, cfg);
+  P.op_base = 0;
+  P.n_ops = dp.n_fused;
+  P.lut_ok = (dp.fused_lut_ok && lut_allowed(cfg)) ? 1u : 0u;
+  P.prog_swap = dp.fused_swap ? 1u : 0u;
   P.reads = dp.d_reads;
   P.writes = dp.d_writes;
   launch(cls, P, st, r.kernels_launched);
   r.device_ms = timer.stop();
   r.wall_time_ns = now_ns() - t0;
-  const Traffic t = analytic_traffic(p);
-  r.bytes_read = t.fused_read;
-  r.bytes_written = t.fused_written;
+  r.bytes_read = dp.traffic.fused_read;
+  r.bytes_written = dp.traffic.fused_written;
   r.passes = 1;
   r.points_visited = uint64_t(p.space.width) * p.space.height * p.space.batch;
   r.path = FK_PATH_GENERIC;
@@ -440,11 +466,13 @@ fk_exec_report execute_unfused(const Pipeline& p, const fk_exec_config* cfg) {
   Timer timer(st, cfg && (cfg->flags & FK_EXEC_TIMED));
   const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
   const size_t n = p.compute.size();
-  const Traffic t = analytic_traffic(p);
   if (n == 0) {  // executor.cpp:144-166: one read -> write sweep
     const int cls = generic_state_class(dp.fused_wide, dp.fused_lanes);
     DPlan P = base_plan(W, H, B, dp.read_flat && dp.write_flat, generic_elems(cls));
-    fill_plan_io(P, dp, p);
+    fill_plan_io(P, dp, p, cfg);
+    P.op_base = 0;
+    P.n_ops = 0;
+    P.lut_ok = lut_allowed(cfg) ? 1u : 0u;  // folded unaries alone
     P.reads = dp.d_reads;
     P.writes = dp.d_writes;
     launch(cls, P, st, r.kernels_launched);
@@ -468,7 +496,8 @@ fk_exec_report execute_unfused(const Pipeline& p, const fk_exec_config* cfg) {
         rd.rect_h = rd.out_h = H;
         rd.kind = prev_kind;
         rd.mode = RD_DIRECT;
-        rd.flags = SF_LANE_ALIGNED;
+        rd.post_off = dp.n_fused + dp.n_ops;
+        rd.flags = SF_LANE_ALIGNED | (lane_kind(prev_kind) == FK_U8 ? SF_LUT_SRC : 0u);
       }
       void* next = nullptr;
       uint32_t out_kind = 0;
@@ -484,7 +513,7 @@ fk_exec_report execute_unfused(const Pipeline& p, const fk_exec_config* cfg) {
       const int cls = generic_state_class(wide, lanes);
       const bool flat = (i == 0 ? dp.read_flat : true) && (final_pass ? dp.write_flat : true);
       DPlan P = base_plan(W, H, B, flat, generic_elems(cls));
-      fill_plan_io(P, dp, p);
+      fill_plan_io(P, dp, p, cfg);
       if (i == 0) {
         P.reads = dp.d_reads;
       } else {
@@ -493,9 +522,13 @@ fk_exec_report execute_unfused(const Pipeline& p, const fk_exec_config* cfg) {
       }
       if (final_pass) {  // final sweep through the write op (executor.cpp:197-213)
         P.writes = dp.d_writes;
+        P.n_ops = 0;
       } else {           // store_block_to the fresh intermediate (executor.cpp:126-130)
-        P.ops = dp.d_ops + i;
+        const DOp& d = dp.table[dp.n_fused + i];
+        P.op_base = dp.n_fused + uint32_t(i);
         P.n_ops = 1;
+        P.lut_ok = (lane_wise(d) && lut_allowed(cfg)) ? 1u : 0u;
+        P.prog_swap = odd_swap(d) ? 1u : 0u;
         P.wr.dst[0] = reinterpret_cast<uint64_t>(next);
         P.wr.pitch[0] = uint64_t(W) * bpe(out_kind);
         P.wr.flags = WF_ACTIVE | WF_LANE_ALIGNED;
@@ -511,8 +544,8 @@ fk_exec_report execute_unfused(const Pipeline& p, const fk_exec_config* cfg) {
   }
   r.device_ms = timer.stop();
   r.wall_time_ns = now_ns() - t0;
-  r.bytes_read = t.unfused_read;
-  r.bytes_written = t.unfused_written;
+  r.bytes_read = dp.traffic.unfused_read;
+  r.bytes_written = dp.traffic.unfused_written;
   r.passes = n + 1;
   r.points_visited = uint64_t(W) * H * B * r.passes;
   r.path = FK_PATH_GENERIC;

@@ -12,12 +12,17 @@
 #include "fk_launch.hpp"
 #include "fk_stages.cuh"
 
+#ifndef FK_MIN_BLOCKS
+#define FK_MIN_BLOCKS 3  // CTAs per SM the register budget must allow
+#endif
+
 namespace fk {
 
 template <class Lane, int L, int E>
-__global__ void __launch_bounds__(kBlock) fk_transform_generic(const __grid_constant__ DPlan P) {
+__global__ void __launch_bounds__(kBlock, FK_MIN_BLOCKS) fk_transform_generic(const __grid_constant__ DPlan P) {
   __shared__ XEnt xt[kXCap];
   __shared__ YEnt yt[kYCap];
+  __shared__ Lane lut[L][256];
   // this CTA walks tiles [t_begin, t_end) of plane z; a tile is E consecutive x of one row
   const uint32_t t_begin = blockIdx.x * P.tiles_per_cta;
   if (t_begin >= P.tiles) return;
@@ -39,11 +44,14 @@ __global__ void __launch_bounds__(kBlock) fk_transform_generic(const __grid_cons
       w = P.wr;
       w.dst[0] += uint64_t(z) * P.wr_zstride;
     }
-    // resampling planes: per-column / per-row coordinates once per CTA (uniform branch)
+    // CTA-uniform setup: resample coordinate tables and the u8 chain LUT
     const bool tab = s.mode != RD_DIRECT && !(s.flags & SF_DEFAULT) && P.width <= kXCap && rows <= kYCap;
-    if (tab) {
+    const bool use_lut = P.lut_ok && (s.flags & SF_LUT_SRC) && (P.n_ops + s.post_len) > 0;
+    const bool swap = ((s.flags & SF_POST_SWAP) != 0) != (P.prog_swap != 0);
+    if (tab || use_lut) {
       __syncthreads();
-      dev::build_tables(s, P.width, y_first, rows, xt, yt);
+      if (tab) dev::build_tables(s, P.width, y_first, rows, xt, yt);
+      if (use_lut) dev::build_lut<Lane, L, E>(P, s, z, lut);
       __syncthreads();
     }
     for (uint32_t t = t_begin + threadIdx.x; t < t_end; t += kBlock) {
@@ -51,10 +59,12 @@ __global__ void __launch_bounds__(kBlock) fk_transform_generic(const __grid_cons
       const uint32_t x = (t - y * P.tiles_per_row) * E;
       const int n = (P.width - x) < uint32_t(E) ? int(P.width - x) : E;
       Lane v[E][L];
-      dev::read_tile(P, s, z, x, y, n, v, tab ? xt : nullptr, tab ? yt + (y - y_first) : nullptr);
-      for (uint32_t i = 0; i < P.n_ops; ++i) {
-        const DOp op = P.ops[i];
-        dev::apply_op(op, z, v);
+      dev::read_raw(P, s, x, y, n, v, tab ? xt : nullptr, tab ? yt + (y - y_first) : nullptr);
+      if (use_lut) {
+        dev::apply_lut(lut, swap, v);
+      } else {
+        if (!(s.flags & SF_DEFAULT)) dev::run_ops(P, s.post_off, s.post_len, z, v);
+        dev::run_ops(P, P.op_base, P.n_ops, z, v);
       }
       dev::write_tile(P, w, x, y, n, v);
     }

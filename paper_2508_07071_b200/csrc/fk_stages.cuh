@@ -180,14 +180,22 @@ __device__ __forceinline__ void load_elem(const uint8_t* p, bool al, Lane (&v)[E
   for (int l = 0; l < T::nl; ++l) v[e][l] = load_lane<T::lk, Lane>(p + l * T::lb, al);
 }
 
-// Two horizontally adjacent u8x3 taps (6 bytes at p) through two aligned 32-bit loads:
-// the 8-byte window [p & ~3, +8) always holds them and never leaves the words that
-// contain in-bounds bytes, so it cannot fault past an allocation.
-__device__ __forceinline__ uint64_t load_u8x3_pair(const uint8_t* p) {
-  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-  const uint32_t* w = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
-  const uint64_t v = uint64_t(__ldg(w)) | (uint64_t(__ldg(w + 1)) << 32);
-  return v >> ((a & 3) * 8);
+// The two u8x3 taps of one source row (3 bytes at o0, 3 bytes at o1, o1 - o0 in
+// {0, 3}) from aligned 32-bit words: the bytes [o0, o1 + 3) lie in at most three
+// words from (row + o0) & ~3, and a word is loaded only if it holds one of those
+// bytes, so the gather never touches memory past the plane.
+__device__ __forceinline__ void load_u8x3_taps(const uint8_t* row, uint32_t o0, uint32_t o1, uint32_t& a,
+                                               uint32_t& b) {
+  const uintptr_t p = reinterpret_cast<uintptr_t>(row + o0);
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(p & ~uintptr_t(3));
+  const uint32_t r = uint32_t(p & 3);
+  const uint32_t last = r + (o1 - o0) + 2;           // relative index of the last byte needed
+  const uint32_t w0 = __ldg(w);
+  const uint32_t w1 = last >= 4 ? __ldg(w + 1) : 0u;
+  const uint32_t w2 = last >= 8 ? __ldg(w + 2) : 0u;
+  const uint32_t sa = 8 * r, sb = 8 * (r + (o1 - o0));
+  a = __funnelshift_r(w0, w1, sa) & 0xffffffu;
+  b = (sb < 32 ? __funnelshift_r(w0, w1, sb) : __funnelshift_r(w1, w2, sb - 32)) & 0xffffffu;
 }
 
 // bilinear_sample, ops.cpp:259-299, for one output pixel whose taps are at byte
@@ -201,23 +209,22 @@ __device__ __forceinline__ void bilinear_px(const uint8_t* r0, const uint8_t* r1
   using T = KindT<K>;
   if constexpr (T::lk == FK_U8) {
     uint32_t ta[T::nl], tb[T::nl], tc[T::nl], td[T::nl];
-    if (T::nl == 3 && o1 == o0 + 3) {
-      const uint64_t top = load_u8x3_pair(r0 + o0), bot = load_u8x3_pair(r1 + o0);
+    if constexpr (T::nl == 3) {
+      uint32_t a, b, c, d;
+      load_u8x3_taps(r0, o0, o1, a, b);
+      load_u8x3_taps(r1, o0, o1, c, d);
 #pragma unroll
-      for (int l = 0; l < T::nl; ++l) {
-        ta[l] = uint32_t(top >> (8 * l)) & 0xffu;
-        tb[l] = uint32_t(top >> (8 * l + 24)) & 0xffu;
-        tc[l] = uint32_t(bot >> (8 * l)) & 0xffu;
-        td[l] = uint32_t(bot >> (8 * l + 24)) & 0xffu;
+      for (int l = 0; l < 3; ++l) {
+        ta[l] = (a >> (8 * l)) & 0xffu;
+        tb[l] = (b >> (8 * l)) & 0xffu;
+        tc[l] = (c >> (8 * l)) & 0xffu;
+        td[l] = (d >> (8 * l)) & 0xffu;
       }
     } else {
-#pragma unroll
-      for (int l = 0; l < T::nl; ++l) {
-        ta[l] = __ldg(r0 + o0 + l);
-        tb[l] = __ldg(r0 + o1 + l);
-        tc[l] = __ldg(r1 + o0 + l);
-        td[l] = __ldg(r1 + o1 + l);
-      }
+      ta[0] = __ldg(r0 + o0);
+      tb[0] = __ldg(r0 + o1);
+      tc[0] = __ldg(r1 + o0);
+      td[0] = __ldg(r1 + o1);
     }
     constexpr double kTwo52 = 4503599627370496.0;        // 2^52
     constexpr double kRound = 6755399441055744.0;        // 1.5 * 2^52
@@ -331,10 +338,25 @@ __device__ __forceinline__ void read_kind(const DSample& s, uint32_t x, uint32_t
   }
 }
 
-// read_exec_block, ops.cpp:361-381, plus the folded unaries (sample_block :343)
+// Program table access: inline in kernel-parameter space (constant bank) when the
+// whole table fits, else HBM.
+__device__ __forceinline__ DOp prog_op(const DPlan& P, uint32_t i) {
+  return P.prog_inline ? P.prog[i] : P.table[i];
+}
+
 template <class Lane, int L, int E>
-__device__ __forceinline__ void read_tile(const DPlan& P, const DSample& s, uint32_t z, uint32_t x, uint32_t y,
-                                          int n, Lane (&v)[E][L], const XEnt* xt, const YEnt* yt) {
+__device__ __forceinline__ void run_ops(const DPlan& P, uint32_t first, uint32_t count, uint32_t z, Lane (&v)[E][L]) {
+  for (uint32_t i = 0; i < count; ++i) {
+    const DOp op = prog_op(P, first + i);
+    apply_op(op, z, v);
+  }
+}
+
+// read_exec_block, ops.cpp:361-381, without the folded unaries (sample_block :343
+// applies them; the caller runs them or their LUT).
+template <class Lane, int L, int E>
+__device__ __forceinline__ void read_raw(const DPlan& P, const DSample& s, uint32_t x, uint32_t y, int n,
+                                         Lane (&v)[E][L], const XEnt* xt, const YEnt* yt) {
   if (s.flags & SF_DEFAULT) {  // z >= active_count: default value, no post ops
 #pragma unroll
     for (int e = 0; e < E; ++e)
@@ -350,9 +372,40 @@ __device__ __forceinline__ void read_tile(const DPlan& P, const DSample& s, uint
     case FK_F32X3: read_kind<FK_F32X3>(s, x, y, n, v, xt, yt); break;
     default: read_kind<FK_F64X3>(s, x, y, n, v, xt, yt); break;
   }
-  for (uint32_t i = 0; i < s.post_len; ++i) {
-    const DOp op = P.post[s.post_off + i];
-    apply_op(op, z, v);
+}
+
+// The folded unaries followed by the compute program, tabulated over the 256
+// values a u8 lane can take (every op involved is lane-wise, so output lane l is
+// g_l(input lane perm(l)) and g_l(t) is the program run on the lane vector (t,t,t)).
+// Each entry is computed by the same device ops as the direct path: bit-exact by
+// construction.
+template <class Lane, int L, int E>
+__device__ __forceinline__ void build_lut(const DPlan& P, const DSample& s, uint32_t z, Lane (*lut)[256]) {
+  for (uint32_t t = threadIdx.x; t < 256; t += blockDim.x) {
+    Lane v[E][L];
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+#pragma unroll
+      for (int l = 0; l < L; ++l) v[e][l] = Lane(t);
+    run_ops(P, s.post_off, s.post_len, z, v);
+    run_ops(P, P.op_base, P.n_ops, z, v);
+#pragma unroll
+    for (int l = 0; l < L; ++l) lut[l][t] = v[0][l];
+  }
+}
+
+template <class Lane, int L, int E>
+__device__ __forceinline__ void apply_lut(const Lane (*lut)[256], bool swap, Lane (&v)[E][L]) {
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    if constexpr (L == 3) {
+      const uint32_t i0 = uint32_t(v[e][0]) & 0xffu, i1 = uint32_t(v[e][1]) & 0xffu, i2 = uint32_t(v[e][2]) & 0xffu;
+      v[e][0] = lut[0][swap ? i2 : i0];
+      v[e][1] = lut[1][i1];
+      v[e][2] = lut[2][swap ? i0 : i2];
+    } else {
+      v[e][0] = lut[0][uint32_t(v[e][0]) & 0xffu];
+    }
   }
 }
 

@@ -234,10 +234,11 @@ class ExecConfig:
     timed: bool = False
     force_generic: bool = False
     serial: bool = False
+    no_lut: bool = False
 
     def c(self) -> _ffi.fk_exec_config:
         flags = ((_ffi.EXEC_TIMED if self.timed else 0) | (_ffi.EXEC_FORCE_GENERIC if self.force_generic else 0)
-                 | (_ffi.EXEC_SERIAL if self.serial else 0))
+                 | (_ffi.EXEC_SERIAL if self.serial else 0) | (_ffi.EXEC_NO_LUT if self.no_lut else 0))
         return _ffi.fk_exec_config(self.workers, self.coarsening, self.chunk_rows, flags, self.stream)
 
 
