@@ -162,6 +162,8 @@ struct DeviceProgram {
   uint32_t n_fused = 0, n_ops = 0;
   bool fused_lut_ok = true;      // every fused op is lane-wise
   bool fused_swap = false;       // odd number of lane swaps in the fused program
+  bool resample_ok = false;      // the compiled u8 resample/LUT kernel can run the fused pass
+  int resample_lanes = 0;
   DSample* d_reads = nullptr;
   DWrite* d_writes = nullptr;
   std::vector<void*> extra;      // BatchArith constant tables
@@ -189,7 +191,26 @@ namespace {
 bool lane_wise(const DOp& d) { return d.cls != OC_GRAY; }
 bool odd_swap(const DOp& d) { return d.cls == OC_SWAP && (d.repeat & 1u); }
 
+// The unfused comparator allocates stream-ordered intermediates every execute
+// (executor.cpp:112-118 allocates fresh planes per pass); keep freed blocks in
+// the device pool instead of returning them to the driver at each sync.
+void keep_pool_memory(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lock(mu);
+  for (int d : done)
+    if (d == device) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t keep = ~uint64_t(0);
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  }
+  cudaGetLastError();
+  done.push_back(device);
+}
+
 std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
+  keep_pool_memory(device);
   auto dp = std::make_shared<DeviceProgram>();
   dp->device = device;
   const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
@@ -308,6 +329,17 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
   if (dp->read_wide) dp->fused_wide = true;
   if (dp->read_lanes == 3) dp->fused_lanes = 3;
 
+  // compiled-kernel eligibility: every plane a u8-lane read with lane-wise folded
+  // unaries, a lane-wise compute program, lane count preserved to the write
+  {
+    bool ok = dp->fused_lut_ok && !dp->reads.empty();
+    const int nl = dp->reads.empty() ? 0 : lanes_of(dp->reads[0].kind);
+    for (const DSample& s : dp->reads)
+      ok = ok && !(s.flags & SF_DEFAULT) && (s.flags & SF_LUT_SRC) && lanes_of(s.kind) == nl;
+    ok = ok && lanes_of(uint32_t(p.write.in_kind)) == nl;
+    dp->resample_ok = ok;
+    dp->resample_lanes = nl;
+  }
   dp->traffic = analytic_traffic(p);
   dp->d_table = upload(dp->table);
   dp->d_reads = upload(dp->reads);
@@ -436,9 +468,10 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
   cudaStream_t st = cfg ? static_cast<cudaStream_t>(cfg->stream) : nullptr;
   fk_exec_report r{};
   Timer timer(st, cfg && (cfg->flags & FK_EXEC_TIMED));
+  const bool compiled = dp.resample_ok && lut_allowed(cfg) && !(cfg && (cfg->flags & FK_EXEC_FORCE_GENERIC));
   const int cls = generic_state_class(dp.fused_wide, dp.fused_lanes);
   DPlan P = base_plan(p.space.width, p.space.height, p.space.batch, dp.read_flat && dp.write_flat,
-                      generic_elems(cls));
+                      compiled ? resample_elems() : generic_elems(cls));
   fill_plan_io(P, dp, p, cfg);
   P.op_base = 0;
   P.n_ops = dp.n_fused;
@@ -446,14 +479,23 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
   P.prog_swap = dp.fused_swap ? 1u : 0u;
   P.reads = dp.d_reads;
   P.writes = dp.d_writes;
-  launch(cls, P, st, r.kernels_launched);
+  if (compiled) {
+    cuda_check(launch_resample(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)), P.write_mode == WR_SPLIT,
+                               P, st),
+               "fk_resample_lut launch");
+    ++r.kernels_launched;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    r.path = FK_PATH_COMPILED;
+  } else {
+    launch(cls, P, st, r.kernels_launched);
+    r.path = FK_PATH_GENERIC;
+  }
   r.device_ms = timer.stop();
   r.wall_time_ns = now_ns() - t0;
   r.bytes_read = dp.traffic.fused_read;
   r.bytes_written = dp.traffic.fused_written;
   r.passes = 1;
   r.points_visited = uint64_t(p.space.width) * p.space.height * p.space.batch;
-  r.path = FK_PATH_GENERIC;
   return r;
 }
 

@@ -13,3 +13,11 @@ int generic_elems(int cls);                     // E: consecutive x per thread
 cudaError_t launch_generic(int cls, const DPlan& P, cudaStream_t st);
 
 }  // namespace fk
+
+namespace fk {
+
+// compiled batched u8 crop/resize -> lane-wise chain (LUT) -> write/split kernel (fk_resample.cu)
+int resample_elems();
+cudaError_t launch_resample(int src_lanes, uint32_t out_lane_kind, bool split, const DPlan& P, cudaStream_t st);
+
+}  // namespace fk
