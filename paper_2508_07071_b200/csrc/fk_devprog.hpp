@@ -68,6 +68,11 @@ struct YEnt { uint64_t r0, r1; double f; };  // tap row byte offsets (y0 + clamp
 constexpr uint32_t kBlock = 256;             // threads per CTA
 constexpr uint32_t kXCap = 1024;             // table path when out_w <= kXCap
 constexpr uint32_t kYCap = 160;              // rows one CTA may span (host keeps tiles_per_cta within it)
+constexpr uint32_t kEdge = 0x80000000u;      // XTab::o flag: the second tap equals the first (clamped edge)
+struct XTab {                                // shared-memory column table, struct-of-arrays
+  alignas(16) uint32_t o[kXCap + 8];         // byte offset of tap 0 within the row | kEdge
+  alignas(16) double f[kXCap + 8];           // fx (bilinear), 0 (nearest)
+};
 
 constexpr uint32_t kProg = 24;  // ops carried in kernel-parameter space (constant bank)
 

@@ -164,6 +164,8 @@ struct DeviceProgram {
   bool fused_swap = false;       // odd number of lane swaps in the fused program
   bool resample_ok = false;      // the compiled u8 resample/LUT kernel can run the fused pass
   int resample_lanes = 0;
+  bool affine_ok = false;        // ... in AFFINE mode: cast u8->f32 then <= 4 f32 arith ops
+  uint32_t aff_base = 0, aff_n = 0;
   DSample* d_reads = nullptr;
   DWrite* d_writes = nullptr;
   std::vector<void*> extra;      // BatchArith constant tables
@@ -339,6 +341,36 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
     ok = ok && lanes_of(uint32_t(p.write.in_kind)) == nl;
     dp->resample_ok = ok;
     dp->resample_lanes = nl;
+    // AFFINE mode: [SwapRB | Cast u8->f32]* (exactly one cast, folded or not), then
+    // only f32 Mul/Add/Sub/Div (no swap after the first one), at most 4 of them.
+    bool aff = ok && lane_kind(uint32_t(p.write.in_kind)) == FK_F32;
+    int post_casts = -1;
+    for (const DSample& s : dp->reads) {
+      int casts = 0;
+      for (uint32_t i = 0; i < s.post_len && aff; ++i) {
+        const DOp& d = dp->table[s.post_off + i];
+        if (d.cls == OC_CAST && d.lk_in == FK_U8 && d.lk_out == FK_F32) ++casts;
+        else if (d.cls != OC_SWAP) aff = false;
+      }
+      if (post_casts >= 0 && casts != post_casts) aff = false;
+      post_casts = casts;
+    }
+    int casts = post_casts < 0 ? 0 : post_casts;
+    std::vector<DOp> arith;
+    for (uint32_t i = 0; i < dp->n_fused && aff; ++i) {
+      const DOp& d = dp->table[i];
+      if (d.cls == OC_CAST && d.lk_in == FK_U8 && d.lk_out == FK_F32 && arith.empty()) ++casts;
+      else if (d.cls == OC_SWAP && arith.empty()) continue;
+      else if (d.cls == OC_ARITH && d.lk_in == FK_F32) arith.push_back(d);
+      else aff = false;
+    }
+    aff = aff && casts == 1 && arith.size() <= size_t(resample_affine_max_ops());
+    dp->affine_ok = aff;
+    if (aff) {
+      dp->aff_base = uint32_t(dp->table.size());
+      dp->aff_n = uint32_t(arith.size());
+      dp->table.insert(dp->table.end(), arith.begin(), arith.end());
+    }
   }
   dp->traffic = analytic_traffic(p);
   dp->d_table = upload(dp->table);
@@ -468,21 +500,23 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
   cudaStream_t st = cfg ? static_cast<cudaStream_t>(cfg->stream) : nullptr;
   fk_exec_report r{};
   Timer timer(st, cfg && (cfg->flags & FK_EXEC_TIMED));
-  const bool compiled = dp.resample_ok && lut_allowed(cfg) && !(cfg && (cfg->flags & FK_EXEC_FORCE_GENERIC));
+  const bool generic_only = cfg && (cfg->flags & FK_EXEC_FORCE_GENERIC);
+  const bool affine = dp.affine_ok && !generic_only;
+  const bool compiled = affine || (dp.resample_ok && lut_allowed(cfg) && !generic_only);
   const int cls = generic_state_class(dp.fused_wide, dp.fused_lanes);
   DPlan P = base_plan(p.space.width, p.space.height, p.space.batch, dp.read_flat && dp.write_flat,
                       compiled ? resample_elems() : generic_elems(cls));
   fill_plan_io(P, dp, p, cfg);
-  P.op_base = 0;
-  P.n_ops = dp.n_fused;
+  P.op_base = affine ? dp.aff_base : 0;
+  P.n_ops = affine ? dp.aff_n : dp.n_fused;
   P.lut_ok = (dp.fused_lut_ok && lut_allowed(cfg)) ? 1u : 0u;
   P.prog_swap = dp.fused_swap ? 1u : 0u;
   P.reads = dp.d_reads;
   P.writes = dp.d_writes;
   if (compiled) {
     cuda_check(launch_resample(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)), P.write_mode == WR_SPLIT,
-                               P, st),
-               "fk_resample_lut launch");
+                               affine, P, st),
+               "fk_resample launch");
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     r.path = FK_PATH_COMPILED;

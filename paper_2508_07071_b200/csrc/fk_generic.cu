@@ -20,7 +20,7 @@ namespace fk {
 
 template <class Lane, int L, int E>
 __global__ void __launch_bounds__(kBlock, FK_MIN_BLOCKS) fk_transform_generic(const __grid_constant__ DPlan P) {
-  __shared__ XEnt xt[kXCap];
+  __shared__ XTab xt;
   __shared__ YEnt yt[kYCap];
   __shared__ Lane lut[L][256];
   // this CTA walks tiles [t_begin, t_end) of plane z; a tile is E consecutive x of one row
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(kBlock, FK_MIN_BLOCKS) fk_transform_generic(co
       const uint32_t x = (t - y * P.tiles_per_row) * E;
       const int n = (P.width - x) < uint32_t(E) ? int(P.width - x) : E;
       Lane v[E][L];
-      dev::read_raw(P, s, x, y, n, v, tab ? xt : nullptr, tab ? yt + (y - y_first) : nullptr);
+      dev::read_raw(P, s, x, y, n, v, tab ? &xt : nullptr, tab ? yt + (y - y_first) : nullptr);
       if (use_lut) {
         dev::apply_lut(lut, swap, v);
       } else {

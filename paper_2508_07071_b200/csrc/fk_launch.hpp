@@ -18,6 +18,8 @@ namespace fk {
 
 // compiled batched u8 crop/resize -> lane-wise chain (LUT) -> write/split kernel (fk_resample.cu)
 int resample_elems();
-cudaError_t launch_resample(int src_lanes, uint32_t out_lane_kind, bool split, const DPlan& P, cudaStream_t st);
+int resample_affine_max_ops();
+cudaError_t launch_resample(int src_lanes, uint32_t out_lane_kind, bool split, bool affine, const DPlan& P,
+                            cudaStream_t st);
 
 }  // namespace fk

@@ -182,18 +182,20 @@ __device__ __forceinline__ void load_elem(const uint8_t* p, bool al, Lane (&v)[E
 
 // The two u8x3 taps of one source row (3 bytes at o0, 3 bytes at o1, o1 - o0 in
 // {0, 3}) from aligned 32-bit words: the bytes [o0, o1 + 3) lie in at most three
-// words from (row + o0) & ~3, and a word is loaded only if it holds one of those
-// bytes, so the gather never touches memory past the plane.
+// words from (row + o0) & ~3. A word that holds none of those bytes is not read
+// (its load is redirected to the first word), so the gather never touches memory
+// past the plane, and it has no branches.
 __device__ __forceinline__ void load_u8x3_taps(const uint8_t* row, uint32_t o0, uint32_t o1, uint32_t& a,
                                                uint32_t& b) {
   const uintptr_t p = reinterpret_cast<uintptr_t>(row + o0);
   const uint32_t* w = reinterpret_cast<const uint32_t*>(p & ~uintptr_t(3));
   const uint32_t r = uint32_t(p & 3);
-  const uint32_t last = r + (o1 - o0) + 2;           // relative index of the last byte needed
+  const uint32_t d = o1 - o0;
+  const uint32_t last = r + d + 2;  // relative index of the last byte needed
   const uint32_t w0 = __ldg(w);
-  const uint32_t w1 = last >= 4 ? __ldg(w + 1) : 0u;
-  const uint32_t w2 = last >= 8 ? __ldg(w + 2) : 0u;
-  const uint32_t sa = 8 * r, sb = 8 * (r + (o1 - o0));
+  const uint32_t w1 = __ldg(w + (last >= 4 ? 1 : 0));
+  const uint32_t w2 = __ldg(w + (last >= 8 ? 2 : 0));
+  const uint32_t sa = 8 * r, sb = 8 * (r + d);
   a = __funnelshift_r(w0, w1, sa) & 0xffffffu;
   b = (sb < 32 ? __funnelshift_r(w0, w1, sb) : __funnelshift_r(w1, w2, sb - 32)) & 0xffffffu;
 }
@@ -291,18 +293,43 @@ __device__ __forceinline__ YEnt y_entry(const DSample& s, uint32_t j) {
   return y;
 }
 
+__device__ __forceinline__ uint32_t kind_bpe(uint32_t k) {
+  return k == FK_U8 ? 1u : k == FK_F32 ? 4u : k == FK_F64 ? 8u : k == FK_U8X3 ? 3u : k == FK_F32X3 ? 12u : 24u;
+}
+
 // Resample tables for this CTA's rows [y_first, y_first + rows) (block-cooperative).
+// The column table is struct-of-arrays so a thread reads its E consecutive
+// entries with 128-bit shared loads: conflict-free across the warp.
 __device__ __forceinline__ void build_tables(const DSample& s, uint32_t width, uint32_t y_first, uint32_t rows,
-                                             XEnt* xt, YEnt* yt) {
-  constexpr uint32_t kBpe[6] = {1, 4, 8, 3, 12, 24};
-  const uint32_t b = kBpe[s.kind];
-  for (uint32_t i = threadIdx.x; i < width; i += blockDim.x) xt[i] = x_entry(s, i, b);
+                                             XTab& xt, YEnt* yt) {
+  const uint32_t b = kind_bpe(s.kind);
+  const uint32_t padded = (width + 7u) & ~7u;
+  for (uint32_t i = threadIdx.x; i < padded; i += blockDim.x) {
+    const XEnt e = x_entry(s, i < width ? i : width - 1, b);
+    xt.o[i] = e.o0 | (e.o1 == e.o0 ? kEdge : 0u);
+    xt.f[i] = e.f;
+  }
   for (uint32_t j = threadIdx.x; j < rows; j += blockDim.x) yt[j] = y_entry(s, y_first + j);
+}
+
+template <int E>
+__device__ __forceinline__ void load_xtab(const XTab& xt, uint32_t x, uint32_t (&o)[E], double (&f)[E]) {
+  static_assert(E % 4 == 0, "tile width must be a multiple of 4");
+#pragma unroll
+  for (int i = 0; i < E / 4; ++i) {
+    const uint4 q = *reinterpret_cast<const uint4*>(&xt.o[x + 4 * i]);
+    o[4 * i] = q.x; o[4 * i + 1] = q.y; o[4 * i + 2] = q.z; o[4 * i + 3] = q.w;
+  }
+#pragma unroll
+  for (int i = 0; i < E / 2; ++i) {
+    const double2 d = *reinterpret_cast<const double2*>(&xt.f[x + 2 * i]);
+    f[2 * i] = d.x; f[2 * i + 1] = d.y;
+  }
 }
 
 template <uint32_t K, class Lane, int L, int E>
 __device__ __forceinline__ void read_kind(const DSample& s, uint32_t x, uint32_t y, int n, Lane (&v)[E][L],
-                                          const XEnt* xt, const YEnt* yt) {
+                                          const XTab* xt, const YEnt* yt) {
   if constexpr (fits<K, Lane, L>()) {
     using T = KindT<K>;
     const bool al = (s.flags & SF_LANE_ALIGNED) != 0;
@@ -327,12 +354,24 @@ __device__ __forceinline__ void read_kind(const DSample& s, uint32_t x, uint32_t
     const YEnt ye = yt ? *yt : y_entry(s, y);
     const uint8_t* r0 = base + ye.r0;
     const uint8_t* r1 = base + ye.r1;
+    uint32_t o[E];
+    double f[E];
+    if (xt) {
+      load_xtab<E>(*xt, x, o, f);
+    } else {
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        const XEnt xe = x_entry(s, x + (e < n ? e : 0), T::bpe);
+        o[e] = xe.o0 | (xe.o1 == xe.o0 ? kEdge : 0u);
+        f[e] = xe.f;
+      }
+    }
 #pragma unroll
     for (int e = 0; e < E; ++e) {
       if (e < n) {
-        const XEnt xe = xt ? xt[x + e] : x_entry(s, x + e, T::bpe);
-        if (s.mode == RD_NEAREST) load_elem<K>(r0 + xe.o0, al, v, e);  // nearest_sample, ops.cpp:301-310
-        else bilinear_px<K>(r0, r1, xe.o0, xe.o1, xe.f, ye.f, al, v, e);
+        const uint32_t o0 = o[e] & ~kEdge, o1 = (o[e] & kEdge) ? o0 : o0 + T::bpe;
+        if (s.mode == RD_NEAREST) load_elem<K>(r0 + o0, al, v, e);  // nearest_sample, ops.cpp:301-310
+        else bilinear_px<K>(r0, r1, o0, o1, f[e], ye.f, al, v, e);
       }
     }
   }
@@ -356,7 +395,7 @@ __device__ __forceinline__ void run_ops(const DPlan& P, uint32_t first, uint32_t
 // applies them; the caller runs them or their LUT).
 template <class Lane, int L, int E>
 __device__ __forceinline__ void read_raw(const DPlan& P, const DSample& s, uint32_t x, uint32_t y, int n,
-                                         Lane (&v)[E][L], const XEnt* xt, const YEnt* yt) {
+                                         Lane (&v)[E][L], const XTab* xt, const YEnt* yt) {
   if (s.flags & SF_DEFAULT) {  // z >= active_count: default value, no post ops
 #pragma unroll
     for (int e = 0; e < E; ++e)

@@ -9,14 +9,14 @@ import pytest
 
 from fkchains import (ChainSpec, ReadSpec, mismatch_report, outputs_equal, random_chain, run)
 from paper_2508_07071_b200._ffi import (BILINEAR, F32, F32X3, NEAREST, OP_ADD, OP_DIV, OP_MUL, OP_SUB, SWAP_RB,
-                                        U8, U8X3, PATH_GENERIC)
+                                        U8, U8X3, PATH_GENERIC, PATH_COMPILED)
 from paper_2508_07071_b200.opfuse import ExecConfig
 
 pytestmark = pytest.mark.gpu
 
 
-def check(cuda, oracle, spec, unfused=False):
-    got, rep = run(cuda, spec, unfused=unfused)
+def check(cuda, oracle, spec, unfused=False, cfg=None):
+    got, rep = run(cuda, spec, unfused=unfused, cfg=cfg)
     want, wrep = run(oracle, spec, unfused=unfused)
     assert outputs_equal(got, want), mismatch_report(got, want)
     assert (rep.bytes_read, rep.bytes_written, rep.passes, rep.points_visited, rep.intermediate_bytes_allocated) == \
@@ -31,6 +31,43 @@ def test_random_chains_fused(cuda, oracle, seed):
         spec = random_chain(rng, allow_batch_arith=True)
         rep = check(cuda, oracle, spec)
         assert rep.kernels_launched == 1
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_random_chains_interpreter_only(cuda, oracle, seed):
+    """Same chains with the compiled kernels and the u8 LUT disabled: the interpreted path alone."""
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(60):
+        spec = random_chain(rng, allow_batch_arith=True)
+        rep = check(cuda, oracle, spec, cfg=ExecConfig(force_generic=True, no_lut=True))
+        assert rep.path == PATH_GENERIC
+
+
+def test_u8_chains_take_compiled_kernels(cuda, oracle):
+    """u8 crop/resize reads with lane-wise chains run the compiled resample kernel (LUT or AFFINE)."""
+    rng = np.random.default_rng(77)
+    frame = rng.integers(0, 256, (97, 131, 3), dtype=np.uint8)
+    gray = rng.integers(0, 256, (60, 70), dtype=np.uint8)
+    norm = [("arith", OP_SUB, F32X3, (123.675, 116.28, 103.53)), ("arith", OP_DIV, F32X3, (58.395, 57.12, 57.375))]
+    cases = [
+        # AFFINE: swap + cast folded, f32 normalise, split
+        ChainSpec([frame], [ReadSpec(0, 3, 4, 50, 60, 37, 29, BILINEAR, [("swap", U8X3), ("cast", U8X3, F32X3)])],
+                  norm, F32X3, split=True),
+        # AFFINE: cast in the compute chain (not folded), packed write, nearest
+        ChainSpec([frame], [ReadSpec(0, 0, 0, 131, 97, 64, 48, NEAREST)], [("cast", U8X3, F32X3)] + norm, F32X3),
+        # LUT: u8 arithmetic with a swap between per-lane constants
+        ChainSpec([frame], [ReadSpec(0, 10, 10, 40, 40, 40, 40, BILINEAR)],
+                  [("arith", OP_MUL, U8X3, (3, 5, 7)), ("swap", U8X3), ("arith", OP_ADD, U8X3, (1, 2, 3))], U8X3),
+        # LUT: gray u8 plane, cast to f64, StaticLoop
+        ChainSpec([gray], [ReadSpec(0, 2, 3, 33, 44, 100, 90, BILINEAR)],
+                  [("cast", U8, F64), ("loop", ("arith", OP_MUL, F64, (1.01,)), 7)], F64),
+        # LUT: direct (non-resizing) crop
+        ChainSpec([frame], [ReadSpec(0, 5, 6, 77, 55)], [("cast", U8X3, F32X3), ("arith", OP_DIV, F32X3, (3.0, 7.0, 9.0))],
+                  F32X3, split=True),
+    ]
+    for spec in cases:
+        rep = check(cuda, oracle, spec)
+        assert rep.path == PATH_COMPILED, spec
 
 
 @pytest.mark.parametrize("seed", range(3))
