@@ -9,6 +9,7 @@
 
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -17,6 +18,7 @@
 #include "fk_core.hpp"
 #include "fk_exec.hpp"
 #include "fk_launch.hpp"
+#include "fk_sig.cuh"
 
 namespace fk {
 
@@ -164,8 +166,9 @@ struct DeviceProgram {
   bool fused_swap = false;       // odd number of lane swaps in the fused program
   bool resample_ok = false;      // the compiled u8 resample/LUT kernel can run the fused pass
   int resample_lanes = 0;
-  bool affine_ok = false;        // ... in AFFINE mode: cast u8->f32 then <= 4 f32 arith ops
-  uint32_t aff_base = 0, aff_n = 0;
+  bool affine_ok = false;        // ... in AFFINE mode: cast u8->f32 then a registered f32 chain
+  uint32_t aff_base = 0, aff_n = 0, aff_sig = 0;
+  std::map<uint64_t, std::vector<uint64_t>> per_z_host;  // BatchArith rows by device address
   DSample* d_reads = nullptr;
   DWrite* d_writes = nullptr;
   std::vector<void*> extra;      // BatchArith constant tables
@@ -192,6 +195,57 @@ namespace {
 
 bool lane_wise(const DOp& d) { return d.cls != OC_GRAY; }
 bool odd_swap(const DOp& d) { return d.cls == OC_SWAP && (d.repeat & 1u); }
+
+float f32_bits(uint64_t v) {
+  float f;
+  const uint32_t b = uint32_t(v);
+  std::memcpy(&f, &b, 4);
+  return f;
+}
+bool same_f32(float a, float b) {
+  if (a != a && b != b) return true;
+  return std::memcmp(&a, &b, 4) == 0;
+}
+
+// The AFFINE chain's op k is a division: does the reciprocal form (fk_sig.cuh
+// div_by_recip) equal IEEE division on every value op k can receive? After a u8
+// read those are prefix_k(t) for t in 0..255, per lane and — with BatchArith
+// constants — per plane: at most 256 * 3 * batch checks, done once per pipeline
+// in host IEEE arithmetic (identical to the device's _rn ops).
+bool recip_div_exact(const std::vector<DOp>& arith, size_t k, const std::map<uint64_t, std::vector<uint64_t>>& rows,
+                     uint32_t batch) {
+  bool per_plane = false;
+  for (size_t j = 0; j <= k; ++j) per_plane = per_plane || arith[j].per_z;
+  const uint32_t planes = per_plane ? batch : 1;
+  auto lane_const = [&](const DOp& d, uint32_t z, int l) {
+    const int li = d.nl == 3 ? l : 0;
+    if (!d.per_z) return f32_bits(d.c[li]);
+    const std::vector<uint64_t>& r = rows.at(d.per_z);
+    const uint32_t zz = z < d.per_z_n ? z : d.per_z_n - 1;
+    return f32_bits(r[3 * size_t(zz) + li]);
+  };
+  for (uint32_t z = 0; z < planes; ++z)
+    for (int l = 0; l < int(arith[k].nl); ++l) {
+      const float d = lane_const(arith[k], z, l);
+      const float r = 1.0f / d;
+      for (int t = 0; t < 256; ++t) {
+        float v = float(t);
+        for (size_t j = 0; j < k; ++j) {
+          const float c = lane_const(arith[j], z, l);
+          switch (arith[j].fn) {
+            case AF_MUL: v = v * c; break;
+            case AF_ADD: v = v + c; break;
+            case AF_SUB: v = v - c; break;
+            default: v = v / c; break;
+          }
+        }
+        const float q = v * r;
+        const float e = std::fmaf(-q, d, v);
+        if (!same_f32(std::fmaf(e, r, q), v / d)) return false;
+      }
+    }
+  return true;
+}
 
 // The unfused comparator allocates stream-ordered intermediates every execute
 // (executor.cpp:112-118 allocates fresh planes per pass); keep freed blocks in
@@ -230,6 +284,7 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
       }
       uint64_t* t = upload(rows);
       dp->extra.push_back(t);
+      dp->per_z_host[reinterpret_cast<uint64_t>(t)] = rows;
       d.per_z = reinterpret_cast<uint64_t>(t);
       d.per_z_n = uint32_t(op.values.size());
     }
@@ -364,9 +419,22 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
       else if (d.cls == OC_ARITH && d.lk_in == FK_F32) arith.push_back(d);
       else aff = false;
     }
-    aff = aff && casts == 1 && arith.size() <= size_t(resample_affine_max_ops());
+    aff = aff && casts == 1 && arith.size() <= 4;
+    for (const DOp& d : arith) aff = aff && d.repeat == 1;
+    uint32_t sig = kSigLut;
+    if (aff) {
+      uint32_t fn[4] = {0, 0, 0, 0}, fast = 0;
+      for (size_t k = 0; k < arith.size(); ++k) {
+        fn[k] = arith[k].fn;
+        if (fn[k] == AF_DIV && recip_div_exact(arith, k, dp->per_z_host, B)) fast |= 1u << k;
+      }
+      sig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast);
+      if (!resample_affine_registered(sig)) sig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], 0);
+      aff = resample_affine_registered(sig);
+    }
     dp->affine_ok = aff;
     if (aff) {
+      dp->aff_sig = sig;
       dp->aff_base = uint32_t(dp->table.size());
       dp->aff_n = uint32_t(arith.size());
       dp->table.insert(dp->table.end(), arith.begin(), arith.end());
@@ -515,7 +583,7 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
   P.writes = dp.d_writes;
   if (compiled) {
     cuda_check(launch_resample(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)), P.write_mode == WR_SPLIT,
-                               affine, P, st),
+                               affine ? dp.aff_sig : kSigLut, P, st),
                "fk_resample launch");
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);

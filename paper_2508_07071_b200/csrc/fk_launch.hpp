@@ -18,8 +18,9 @@ namespace fk {
 
 // compiled batched u8 crop/resize -> lane-wise chain (LUT) -> write/split kernel (fk_resample.cu)
 int resample_elems();
-int resample_affine_max_ops();
-cudaError_t launch_resample(int src_lanes, uint32_t out_lane_kind, bool split, bool affine, const DPlan& P,
+bool resample_affine_registered(uint32_t sig);  // fk_sig.cuh FK_AFFINE_SIGS
+// sig == kSigLut: LUT mode; else the registered AFFINE chain signature
+cudaError_t launch_resample(int src_lanes, uint32_t out_lane_kind, bool split, uint32_t sig, const DPlan& P,
                             cudaStream_t st);
 
 }  // namespace fk

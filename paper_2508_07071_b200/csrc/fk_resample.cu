@@ -12,9 +12,11 @@
 // run once per column/row instead of once per pixel.
 //
 // Two chain modes, picked on the host:
-//  * AFFINE: Cast(u8 -> f32) [+ SwapRB] then <= 4 f32 Mul/Add/Sub/Div ops with
-//    per-lane (and optionally per-plane) constants, evaluated in registers with
-//    the reference's IEEE ops (the normalisation chain of configs[1,3,4]).
+//  * AFFINE: Cast(u8 -> f32) [+ SwapRB] then a registered straight-line chain of
+//    f32 Mul/Add/Sub/Div (fk_sig.cuh), compiled into the kernel as a template
+//    signature, constants per lane (and optionally per plane) in registers —
+//    the normalisation chain of configs[1,3,4]. A division whose reciprocal form
+//    the host verified on all 256 reachable inputs uses it (3 FP32 ops).
 //  * LUT: any lane-wise chain (folded unaries + Cast / arith / SwapRB /
 //    StaticLoop / BatchArith, any length): after a u8 read each output lane is
 //    a function of one byte, so the chain is evaluated once per byte value
@@ -25,14 +27,14 @@
 #include <type_traits>
 
 #include "fk_launch.hpp"
+#include "fk_sig.cuh"
 #include "fk_stages.cuh"
 
 namespace fk {
 
 namespace {
 
-constexpr int kE = 4;      // output pixels per tile (one 16-byte f32 store per planar lane)
-constexpr int kAffOps = 4;  // AFFINE mode: max f32 ops after the cast
+constexpr int kE = 4;  // output pixels per tile (one 16-byte f32 store per planar lane)
 
 // The sampled u8 lanes of one output pixel: taps at byte offsets o0/o1 of the
 // rows r0/r1 (bilinear_sample, ops.cpp:259-299) or one tap at o0 of r0.
@@ -79,19 +81,11 @@ __device__ __forceinline__ void sample_u8(bool bilinear, const uint8_t* r0, cons
   }
 }
 
-__device__ __forceinline__ float aff_op(uint32_t fn, float a, float c) {
-  switch (fn) {
-    case AF_MUL: return __fmul_rn(a, c);
-    case AF_ADD: return __fadd_rn(a, c);
-    case AF_SUB: return __fsub_rn(a, c);
-    default: return __fdiv_rn(a, c);
-  }
-}
-
 }  // namespace
 
-template <int NL, uint32_t OLK, bool SPLIT, bool AFFINE>
+template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG>
 __global__ void __launch_bounds__(kBlock, 3) fk_resample(const __grid_constant__ DPlan P) {
+  constexpr bool AFFINE = SIG != kSigLut;
   using Out = typename std::conditional<OLK == FK_F64, uint64_t, uint32_t>::type;
   constexpr int OB = OLK == FK_U8 ? 1 : (OLK == FK_F32 ? 4 : 8);  // bytes per output lane
   __shared__ XTab xt;
@@ -110,22 +104,21 @@ __global__ void __launch_bounds__(kBlock, 3) fk_resample(const __grid_constant__
     const uint8_t* base = reinterpret_cast<const uint8_t*>(s.src);
     const bool resampling = s.mode != RD_DIRECT;
     const bool bilinear = s.mode == RD_BILINEAR;
-    // AFFINE: the f32 ops' constants of plane z in registers (BatchArith rows are per z)
-    uint32_t afn[kAffOps] = {0, 0, 0, 0};
-    float acst[kAffOps][3];
+    // AFFINE: the chain's constants (and reciprocals) of plane z in registers
+    float acst[4][3], arcp[4][3];
     if constexpr (AFFINE) {
 #pragma unroll
-      for (int k = 0; k < kAffOps; ++k) {
-        if (k < int(P.n_ops)) {
-          const DOp op = dev::prog_op(P, P.op_base + k);
-          uint64_t c[3] = {op.c[0], op.c[1], op.c[2]};
-          if (op.per_z) {
-            const uint64_t* row = reinterpret_cast<const uint64_t*>(op.per_z) + 3ull * (z < op.per_z_n ? z : op.per_z_n - 1);
-            c[0] = __ldg(row); c[1] = __ldg(row + 1); c[2] = __ldg(row + 2);
-          }
-          afn[k] = op.fn;
+      for (int k = 0; k < sig_n(SIG); ++k) {
+        const DOp op = dev::prog_op(P, P.op_base + k);
+        uint64_t c[3] = {op.c[0], op.c[1], op.c[2]};
+        if (op.per_z) {
+          const uint64_t* row = reinterpret_cast<const uint64_t*>(op.per_z) + 3ull * (z < op.per_z_n ? z : op.per_z_n - 1);
+          c[0] = __ldg(row); c[1] = __ldg(row + 1); c[2] = __ldg(row + 2);
+        }
 #pragma unroll
-          for (int l = 0; l < 3; ++l) acst[k][l] = __uint_as_float(uint32_t(c[op.nl == 3 ? l : 0]));
+        for (int l = 0; l < 3; ++l) {
+          acst[k][l] = __uint_as_float(uint32_t(c[op.nl == 3 ? l : 0]));
+          arcp[k][l] = __frcp_rn(acst[k][l]);
         }
       }
     }
@@ -183,11 +176,14 @@ __global__ void __launch_bounds__(kBlock, 3) fk_resample(const __grid_constant__
         if constexpr (AFFINE) {
 #pragma unroll
           for (int l = 0; l < NL; ++l) {
-            float v = float(u[l]);  // Cast u8 -> f32: exact
+            float c[4], r[4];
 #pragma unroll
-            for (int k = 0; k < kAffOps; ++k)
-              if (k < int(P.n_ops)) v = aff_op(afn[k], v, acst[k][l]);
-            out[e][l] = Out(__float_as_uint(v));
+            for (int k = 0; k < 4; ++k) {
+              c[k] = k < sig_n(SIG) ? acst[k][l] : 0.f;
+              r[k] = k < sig_n(SIG) ? arcp[k][l] : 0.f;
+            }
+            // Cast u8 -> f32 (exact), then the compiled chain
+            out[e][l] = Out(__float_as_uint(sig_apply<SIG>(float(u[l]), c, r)));
           }
         } else {
 #pragma unroll
@@ -229,34 +225,45 @@ __global__ void __launch_bounds__(kBlock, 3) fk_resample(const __grid_constant__
 }
 
 int resample_elems() { return kE; }
-int resample_affine_max_ops() { return kAffOps; }
 
-cudaError_t launch_resample(int src_lanes, uint32_t out_lane_kind, bool split, bool affine, const DPlan& P,
+bool resample_affine_registered(uint32_t sig) {
+#define FK_CASE(S) if (sig == (S)) return true;
+  FK_AFFINE_SIGS(FK_CASE)
+#undef FK_CASE
+  return false;
+}
+
+cudaError_t launch_resample(int src_lanes, uint32_t out_lane_kind, bool split, uint32_t sig, const DPlan& P,
                             cudaStream_t st) {
   if (P.tiles == 0 || P.batch == 0) return cudaSuccess;
   const dim3 grid((P.tiles + P.tiles_per_cta - 1) / P.tiles_per_cta, 1, P.batch < 65535u ? P.batch : 65535u);
-#define FK_RS(NL, OLK, SP, AF) fk_resample<NL, OLK, SP, AF><<<grid, kBlock, 0, st>>>(P)
-  if (affine) {  // f32 outputs only
-    if (src_lanes == 3) {
-      if (split) FK_RS(3, FK_F32, true, true);
-      else FK_RS(3, FK_F32, false, true);
-    } else {
-      FK_RS(1, FK_F32, false, true);
-    }
-  } else if (src_lanes == 3) {
+#define FK_RS(NL, OLK, SP, S) fk_resample<NL, OLK, SP, S><<<grid, kBlock, 0, st>>>(P)
+  if (sig != kSigLut) {  // AFFINE: f32 outputs
+#define FK_CASE(S)                                   \
+  if (sig == (S)) {                                  \
+    if (src_lanes == 3 && split) FK_RS(3, FK_F32, true, S);        \
+    else if (src_lanes == 3) FK_RS(3, FK_F32, false, S);           \
+    else FK_RS(1, FK_F32, false, S);                                \
+    return cudaGetLastError();                       \
+  }
+    FK_AFFINE_SIGS(FK_CASE)
+#undef FK_CASE
+    return cudaErrorInvalidValue;  // unregistered signature: the host picks LUT mode instead
+  }
+  if (src_lanes == 3) {
     if (split) {
-      if (out_lane_kind == FK_U8) FK_RS(3, FK_U8, true, false);
-      else if (out_lane_kind == FK_F32) FK_RS(3, FK_F32, true, false);
-      else FK_RS(3, FK_F64, true, false);
+      if (out_lane_kind == FK_U8) FK_RS(3, FK_U8, true, kSigLut);
+      else if (out_lane_kind == FK_F32) FK_RS(3, FK_F32, true, kSigLut);
+      else FK_RS(3, FK_F64, true, kSigLut);
     } else {
-      if (out_lane_kind == FK_U8) FK_RS(3, FK_U8, false, false);
-      else if (out_lane_kind == FK_F32) FK_RS(3, FK_F32, false, false);
-      else FK_RS(3, FK_F64, false, false);
+      if (out_lane_kind == FK_U8) FK_RS(3, FK_U8, false, kSigLut);
+      else if (out_lane_kind == FK_F32) FK_RS(3, FK_F32, false, kSigLut);
+      else FK_RS(3, FK_F64, false, kSigLut);
     }
   } else {
-    if (out_lane_kind == FK_U8) FK_RS(1, FK_U8, false, false);
-    else if (out_lane_kind == FK_F32) FK_RS(1, FK_F32, false, false);
-    else FK_RS(1, FK_F64, false, false);
+    if (out_lane_kind == FK_U8) FK_RS(1, FK_U8, false, kSigLut);
+    else if (out_lane_kind == FK_F32) FK_RS(1, FK_F32, false, kSigLut);
+    else FK_RS(1, FK_F64, false, kSigLut);
   }
 #undef FK_RS
   return cudaGetLastError();
