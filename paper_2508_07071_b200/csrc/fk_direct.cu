@@ -1,0 +1,135 @@
+// fk_direct.cu — compiled kernel for element-wise f32 chains (vertical fusion,
+// PAPER.md:530-541; configs[0] and configs[2]).
+//
+//   Read f32 (PerThreadRead / Crop, any batch) -> registered chain of f32
+//   Mul/Add/Sub/Div, each with a runtime StaticLoop repeat count
+//   -> [Cast f32 -> u8] -> Write (f32 or u8)
+//
+// The op sequence is a template signature (fk_sig.cuh) — the kernel is the
+// paper's variadic fused kernel for that chain, constants and repeat counts in
+// kernel parameters. Each thread owns 16 consecutive elements: four 128-bit
+// loads, the chain in registers, one 128-bit (u8) or four (f32) streaming stores.
+#include <cuda_runtime.h>
+
+#include "fk_launch.hpp"
+#include "fk_sig.cuh"
+#include "fk_stages.cuh"
+
+namespace fk {
+
+namespace {
+
+constexpr int kD = 16;  // elements per thread
+
+#define FK_DIRECT_SIGS(X)                                                           \
+  X(sig_make(0)) X(sig_make(1, AF_MUL)) X(sig_make(1, AF_ADD)) X(sig_make(1, AF_SUB)) \
+  X(sig_make(1, AF_DIV)) X(sig_make(2, AF_MUL, AF_ADD)) X(sig_make(2, AF_SUB, AF_DIV)) \
+  X(sig_make(3, AF_MUL, AF_SUB, AF_DIV)) X(sig_make(4, AF_MUL, AF_ADD, AF_SUB, AF_DIV))
+
+template <uint32_t SIG, int K>
+__device__ __forceinline__ void direct_op(float (&v)[kD], float c, uint32_t reps) {
+  if constexpr (K < sig_n(SIG)) {
+#pragma unroll 1
+    for (uint32_t r = 0; r < reps; ++r)
+#pragma unroll
+      for (int e = 0; e < kD; ++e) v[e] = sig_op<SIG, K>(v[e], c, 0.f);
+  }
+}
+
+}  // namespace
+
+template <uint32_t SIG, bool TO_U8>
+__global__ void __launch_bounds__(kBlock) fk_direct(const __grid_constant__ DPlan P) {
+  const uint32_t t_begin = blockIdx.x * P.tiles_per_cta;
+  if (t_begin >= P.tiles) return;
+  const uint32_t t_end = min(t_begin + P.tiles_per_cta, P.tiles);
+  float c[4] = {0.f, 0.f, 0.f, 0.f};
+  uint32_t rep[4] = {0, 0, 0, 0};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k < sig_n(SIG)) {
+      const DOp op = dev::prog_op(P, P.op_base + k);
+      c[k] = __uint_as_float(uint32_t(op.c[0]));
+      rep[k] = op.repeat;
+    }
+  }
+  for (uint32_t z = blockIdx.z; z < P.batch; z += gridDim.z) {
+    const DSample s = P.reads[z];
+    const DWrite w = P.writes[z];
+    if (!(w.flags & WF_ACTIVE)) continue;
+    const bool st = (w.flags & WF_STREAM) != 0;
+    for (uint32_t t = t_begin + threadIdx.x; t < t_end; t += kBlock) {
+      const uint32_t y = dev::fastdiv(t, P.tpr);
+      const uint32_t x = (t - y * P.tiles_per_row) * kD;
+      const int n = (P.width - x) < uint32_t(kD) ? int(P.width - x) : kD;
+      const uint8_t* p = reinterpret_cast<const uint8_t*>(s.src) + uint64_t(s.y0 + y) * s.pitch +
+                         uint64_t(s.x0 + x) * 4;
+      float v[kD];
+      if (n == kD && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+        for (int i = 0; i < kD / 4; ++i) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(p) + i);
+          v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < kD; ++e) v[e] = e < n ? __ldg(reinterpret_cast<const float*>(p) + e) : 0.f;
+      }
+      direct_op<SIG, 0>(v, c[0], rep[0]);
+      direct_op<SIG, 1>(v, c[1], rep[1]);
+      direct_op<SIG, 2>(v, c[2], rep[2]);
+      direct_op<SIG, 3>(v, c[3], rep[3]);
+      uint8_t* q = reinterpret_cast<uint8_t*>(w.dst[0]) + uint64_t(y) * w.pitch[0];
+      if constexpr (TO_U8) {  // Cast f32 -> u8: round_clamp_u8 (scalar.hpp:161-167), rint(f) == rint((double)f)
+        uint32_t b[kD];
+#pragma unroll
+        for (int e = 0; e < kD; ++e) b[e] = dev::round_clamp_u8(v[e]);
+        q += x;
+        if (n == kD && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+          uint32_t wd[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            wd[i] = b[4 * i] | (b[4 * i + 1] << 8) | (b[4 * i + 2] << 16) | (b[4 * i + 3] << 24);
+          dev::store_words<4>(q, wd, st);
+        } else {
+          for (int e = 0; e < n; ++e) q[e] = uint8_t(b[e]);
+        }
+      } else {
+        q += uint64_t(x) * 4;
+        if (n == kD && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+          uint32_t wd[kD];
+#pragma unroll
+          for (int e = 0; e < kD; ++e) wd[e] = __float_as_uint(v[e]);
+          dev::store_words<kD>(q, wd, st);
+        } else {
+          for (int e = 0; e < n; ++e) reinterpret_cast<float*>(q)[e] = v[e];
+        }
+      }
+    }
+  }
+}
+
+int direct_elems() { return kD; }
+
+bool direct_registered(uint32_t sig) {
+#define FK_CASE(S) if (sig == (S)) return true;
+  FK_DIRECT_SIGS(FK_CASE)
+#undef FK_CASE
+  return false;
+}
+
+cudaError_t launch_direct(uint32_t sig, bool to_u8, const DPlan& P, cudaStream_t st) {
+  if (P.tiles == 0 || P.batch == 0) return cudaSuccess;
+  const dim3 grid((P.tiles + P.tiles_per_cta - 1) / P.tiles_per_cta, 1, P.batch < 65535u ? P.batch : 65535u);
+#define FK_CASE(S)                                                          \
+  if (sig == (S)) {                                                         \
+    if (to_u8) fk_direct<S, true><<<grid, kBlock, 0, st>>>(P);              \
+    else fk_direct<S, false><<<grid, kBlock, 0, st>>>(P);                   \
+    return cudaGetLastError();                                              \
+  }
+  FK_DIRECT_SIGS(FK_CASE)
+#undef FK_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace fk

@@ -168,6 +168,9 @@ struct DeviceProgram {
   int resample_lanes = 0;
   bool affine_ok = false;        // ... in AFFINE mode: cast u8->f32 then a registered f32 chain
   uint32_t aff_base = 0, aff_n = 0, aff_sig = 0;
+  bool direct_ok = false;        // the compiled f32 element-wise kernel can run the fused pass
+  bool direct_u8 = false;        // ... ending in Cast f32 -> u8
+  uint32_t dir_base = 0, dir_sig = 0;
   std::map<uint64_t, std::vector<uint64_t>> per_z_host;  // BatchArith rows by device address
   DSample* d_reads = nullptr;
   DWrite* d_writes = nullptr;
@@ -440,6 +443,38 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
       dp->table.insert(dp->table.end(), arith.begin(), arith.end());
     }
   }
+  // direct f32 kernel: f32 planes read as-is, f32 arith runs (any repeat), an
+  // optional final Cast f32 -> u8, a packed write
+  {
+    bool ok = !dp->reads.empty() && (p.write.id == FK_OP_BATCH_WRITE ? p.write.w_inner : p.write.id) ==
+                                        FK_OP_PER_THREAD_WRITE;
+    for (const DSample& s : dp->reads)
+      ok = ok && !(s.flags & SF_DEFAULT) && s.mode == RD_DIRECT && s.kind == FK_F32 && s.post_len == 0 &&
+           (s.flags & SF_LANE_ALIGNED);
+    std::vector<DOp> arith;
+    bool to_u8 = false;
+    for (uint32_t i = 0; i < dp->n_fused && ok; ++i) {
+      const DOp& d = dp->table[i];
+      if (d.cls == OC_ARITH && d.lk_in == FK_F32 && d.nl == 1 && !d.per_z && !to_u8) arith.push_back(d);
+      else if (d.cls == OC_CAST && d.lk_in == FK_F32 && d.lk_out == FK_U8 && d.nl == 1 && i + 1 == dp->n_fused)
+        to_u8 = true;
+      else ok = false;
+    }
+    ok = ok && arith.size() <= 4 && uint32_t(p.write.in_kind) == (to_u8 ? FK_U8 : FK_F32);
+    if (ok) {
+      uint32_t fn[4] = {0, 0, 0, 0};
+      for (size_t k = 0; k < arith.size(); ++k) fn[k] = arith[k].fn;
+      const uint32_t sig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], 0);
+      ok = direct_registered(sig);
+      if (ok) {
+        dp->direct_ok = true;
+        dp->direct_u8 = to_u8;
+        dp->dir_sig = sig;
+        dp->dir_base = uint32_t(dp->table.size());
+        dp->table.insert(dp->table.end(), arith.begin(), arith.end());
+      }
+    }
+  }
   dp->traffic = analytic_traffic(p);
   dp->d_table = upload(dp->table);
   dp->d_reads = upload(dp->reads);
@@ -569,19 +604,26 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
   fk_exec_report r{};
   Timer timer(st, cfg && (cfg->flags & FK_EXEC_TIMED));
   const bool generic_only = cfg && (cfg->flags & FK_EXEC_FORCE_GENERIC);
-  const bool affine = dp.affine_ok && !generic_only;
-  const bool compiled = affine || (dp.resample_ok && lut_allowed(cfg) && !generic_only);
+  // kernel selection: a registered compiled chain first, the interpreter otherwise
+  const bool direct = dp.direct_ok && !generic_only;
+  const bool affine = !direct && dp.affine_ok && !generic_only;
+  const bool compiled = affine || (!direct && dp.resample_ok && lut_allowed(cfg) && !generic_only);
   const int cls = generic_state_class(dp.fused_wide, dp.fused_lanes);
   DPlan P = base_plan(p.space.width, p.space.height, p.space.batch, dp.read_flat && dp.write_flat,
-                      compiled ? resample_elems() : generic_elems(cls));
+                      direct ? direct_elems() : compiled ? resample_elems() : generic_elems(cls));
   fill_plan_io(P, dp, p, cfg);
-  P.op_base = affine ? dp.aff_base : 0;
+  P.op_base = affine ? dp.aff_base : direct ? dp.dir_base : 0;
   P.n_ops = affine ? dp.aff_n : dp.n_fused;
   P.lut_ok = (dp.fused_lut_ok && lut_allowed(cfg)) ? 1u : 0u;
   P.prog_swap = dp.fused_swap ? 1u : 0u;
   P.reads = dp.d_reads;
   P.writes = dp.d_writes;
-  if (compiled) {
+  if (direct) {
+    cuda_check(launch_direct(dp.dir_sig, dp.direct_u8, P, st), "fk_direct launch");
+    ++r.kernels_launched;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    r.path = FK_PATH_COMPILED;
+  } else if (compiled) {
     cuda_check(launch_resample(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)), P.write_mode == WR_SPLIT,
                                affine ? dp.aff_sig : kSigLut, P, st),
                "fk_resample launch");

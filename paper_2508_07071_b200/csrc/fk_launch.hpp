@@ -18,6 +18,11 @@ namespace fk {
 
 // compiled batched u8 crop/resize -> lane-wise chain (LUT) -> write/split kernel (fk_resample.cu)
 int resample_elems();
+// compiled f32 element-wise chain kernel (fk_direct.cu)
+int direct_elems();
+bool direct_registered(uint32_t sig);
+cudaError_t launch_direct(uint32_t sig, bool to_u8, const DPlan& P, cudaStream_t st);
+
 bool resample_affine_registered(uint32_t sig);  // fk_sig.cuh FK_AFFINE_SIGS
 // sig == kSigLut: LUT mode; else the registered AFFINE chain signature
 cudaError_t launch_resample(int src_lanes, uint32_t out_lane_kind, bool split, uint32_t sig, const DPlan& P,

@@ -8,8 +8,8 @@ import numpy as np
 import pytest
 
 from fkchains import (ChainSpec, ReadSpec, mismatch_report, outputs_equal, random_chain, run)
-from paper_2508_07071_b200._ffi import (BILINEAR, F32, F32X3, NEAREST, OP_ADD, OP_DIV, OP_MUL, OP_SUB, SWAP_RB,
-                                        U8, U8X3, PATH_GENERIC, PATH_COMPILED)
+from paper_2508_07071_b200._ffi import (BILINEAR, F32, F32X3, F64, NEAREST, OP_ADD, OP_DIV, OP_MUL, OP_SUB,
+                                        SWAP_RB, U8, U8X3, PATH_GENERIC, PATH_COMPILED)
 from paper_2508_07071_b200.opfuse import ExecConfig
 
 pytestmark = pytest.mark.gpu
@@ -93,8 +93,15 @@ def test_c1_vertical_chain_small(cuda, oracle):
     spec = ChainSpec([src], [ReadSpec(0)],
                      [("arith", OP_MUL, F32, (400.0,)), ("arith", OP_ADD, F32, (2.0,)),
                       ("arith", OP_SUB, F32, (1.5,)), ("arith", OP_DIV, F32, (1.25,)), ("cast", F32, U8)], U8)
-    check(cuda, oracle, spec)
+    assert check(cuda, oracle, spec).path == PATH_COMPILED          # fk_direct<MUL,ADD,SUB,DIV; ->u8>
+    assert check(cuda, oracle, spec, cfg=ExecConfig(force_generic=True)).path == PATH_GENERIC
     check(cuda, oracle, spec, unfused=True)
+    # odd widths, a crop view and f32 output exercise the tails of the 16-wide tiles
+    src2 = rng.random((33, 101), dtype=np.float32) * 300 - 20
+    for rd in (ReadSpec(0), ReadSpec(0, 3, 2, 77, 29)):
+        for comp, wk in (([("arith", OP_MUL, F32, (3.0,)), ("arith", OP_ADD, F32, (0.5,))], F32),
+                         ([("arith", OP_SUB, F32, (7.0,)), ("arith", OP_DIV, F32, (3.0,)), ("cast", F32, U8)], U8)):
+            assert check(cuda, oracle, ChainSpec([src2], [rd], comp, wk, dst_stride_pad=3)).path == PATH_COMPILED
 
 
 def test_cvgs_batch_50(cuda, oracle):
