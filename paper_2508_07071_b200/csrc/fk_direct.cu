@@ -9,7 +9,15 @@
 // paper's variadic fused kernel for that chain, constants and repeat counts in
 // kernel parameters. Each thread owns 16 consecutive elements: four 128-bit
 // loads, the chain in registers, one 128-bit (u8) or four (f32) streaming stores.
+//
+// Division by a constant d uses r = RN(1/d) and one FMA correction
+// (div_guarded) once fk_verify_recip_div has proven, on all 2^32 f32 inputs,
+// that it returns exactly __fdiv_rn(x, d) for this d; otherwise IEEE division.
 #include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <mutex>
 
 #include "fk_launch.hpp"
 #include "fk_sig.cuh"
@@ -21,19 +29,36 @@ namespace {
 
 constexpr int kD = 16;  // elements per thread
 
-#define FK_DIRECT_SIGS(X)                                                           \
-  X(sig_make(0)) X(sig_make(1, AF_MUL)) X(sig_make(1, AF_ADD)) X(sig_make(1, AF_SUB)) \
-  X(sig_make(1, AF_DIV)) X(sig_make(2, AF_MUL, AF_ADD)) X(sig_make(2, AF_SUB, AF_DIV)) \
-  X(sig_make(3, AF_MUL, AF_SUB, AF_DIV)) X(sig_make(4, AF_MUL, AF_ADD, AF_SUB, AF_DIV))
+// registered chains; bit 12+k marks op k as a verified reciprocal division
+#define FK_DIRECT_SIGS(X)                                                                         \
+  X(sig_make(0)) X(sig_make(1, AF_MUL)) X(sig_make(1, AF_ADD)) X(sig_make(1, AF_SUB))               \
+  X(sig_make(1, AF_DIV)) X(sig_make(1, AF_DIV, 0, 0, 0, 1)) X(sig_make(2, AF_MUL, AF_ADD))          \
+  X(sig_make(2, AF_SUB, AF_DIV)) X(sig_make(2, AF_SUB, AF_DIV, 0, 0, 2))                            \
+  X(sig_make(3, AF_MUL, AF_SUB, AF_DIV)) X(sig_make(3, AF_MUL, AF_SUB, AF_DIV, 0, 4))               \
+  X(sig_make(4, AF_MUL, AF_ADD, AF_SUB, AF_DIV)) X(sig_make(4, AF_MUL, AF_ADD, AF_SUB, AF_DIV, 8))
 
 template <uint32_t SIG, int K>
-__device__ __forceinline__ void direct_op(float (&v)[kD], float c, uint32_t reps) {
+__device__ __forceinline__ float direct_elem(float v, float c, float r) {
+  if constexpr (sig_fn(SIG, K) == AF_DIV && sig_fast(SIG, K)) return div_guarded(v, c, r);
+  else return sig_op<SIG, K>(v, c, r);
+}
+
+template <uint32_t SIG, int K>
+__device__ __forceinline__ void direct_op(float (&v)[kD], float c, float r, uint32_t reps) {
   if constexpr (K < sig_n(SIG)) {
 #pragma unroll 1
-    for (uint32_t r = 0; r < reps; ++r)
+    for (uint32_t i = 0; i < reps; ++i)
 #pragma unroll
-      for (int e = 0; e < kD; ++e) v[e] = sig_op<SIG, K>(v[e], c, 0.f);
+      for (int e = 0; e < kD; ++e) v[e] = direct_elem<SIG, K>(v[e], c, r);
   }
+}
+
+// round_clamp_u8 (scalar.hpp:161-167) in one instruction: cvt.rni.sat rounds to
+// nearest-even, saturates to [0, 255] and maps NaN to 0.
+__device__ __forceinline__ uint32_t f32_to_u8(float x) {
+  uint32_t r;
+  asm("cvt.rni.sat.u8.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r & 0xffu;
 }
 
 }  // namespace
@@ -43,13 +68,14 @@ __global__ void __launch_bounds__(kBlock) fk_direct(const __grid_constant__ DPla
   const uint32_t t_begin = blockIdx.x * P.tiles_per_cta;
   if (t_begin >= P.tiles) return;
   const uint32_t t_end = min(t_begin + P.tiles_per_cta, P.tiles);
-  float c[4] = {0.f, 0.f, 0.f, 0.f};
+  float c[4] = {0.f, 0.f, 0.f, 0.f}, r[4] = {0.f, 0.f, 0.f, 0.f};
   uint32_t rep[4] = {0, 0, 0, 0};
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     if (k < sig_n(SIG)) {
       const DOp op = dev::prog_op(P, P.op_base + k);
       c[k] = __uint_as_float(uint32_t(op.c[0]));
+      r[k] = __frcp_rn(c[k]);
       rep[k] = op.repeat;
     }
   }
@@ -75,15 +101,15 @@ __global__ void __launch_bounds__(kBlock) fk_direct(const __grid_constant__ DPla
 #pragma unroll
         for (int e = 0; e < kD; ++e) v[e] = e < n ? __ldg(reinterpret_cast<const float*>(p) + e) : 0.f;
       }
-      direct_op<SIG, 0>(v, c[0], rep[0]);
-      direct_op<SIG, 1>(v, c[1], rep[1]);
-      direct_op<SIG, 2>(v, c[2], rep[2]);
-      direct_op<SIG, 3>(v, c[3], rep[3]);
+      direct_op<SIG, 0>(v, c[0], r[0], rep[0]);
+      direct_op<SIG, 1>(v, c[1], r[1], rep[1]);
+      direct_op<SIG, 2>(v, c[2], r[2], rep[2]);
+      direct_op<SIG, 3>(v, c[3], r[3], rep[3]);
       uint8_t* q = reinterpret_cast<uint8_t*>(w.dst[0]) + uint64_t(y) * w.pitch[0];
-      if constexpr (TO_U8) {  // Cast f32 -> u8: round_clamp_u8 (scalar.hpp:161-167), rint(f) == rint((double)f)
+      if constexpr (TO_U8) {
         uint32_t b[kD];
 #pragma unroll
-        for (int e = 0; e < kD; ++e) b[e] = dev::round_clamp_u8(v[e]);
+        for (int e = 0; e < kD; ++e) b[e] = f32_to_u8(v[e]);
         q += x;
         if (n == kD && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
           uint32_t wd[4];
@@ -107,6 +133,45 @@ __global__ void __launch_bounds__(kBlock) fk_direct(const __grid_constant__ DPla
       }
     }
   }
+}
+
+// Exhaustive proof for one divisor: div_guarded(x, d, RN(1/d)) == __fdiv_rn(x, d)
+// for every one of the 2^32 f32 bit patterns x (NaN results compare equal).
+__global__ void fk_verify_recip_div(float d, unsigned int* bad) {
+  const float r = __frcp_rn(d);
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  unsigned int found = 0;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < (uint64_t(1) << 32); i += stride) {
+    const float x = __uint_as_float(uint32_t(i));
+    const float a = div_guarded(x, d, r), b = __fdiv_rn(x, d);
+    if (__float_as_uint(a) != __float_as_uint(b) && !(isnan(a) && isnan(b))) found = 1;
+  }
+  if (found) atomicOr(bad, 1u);
+}
+
+bool recip_div_verified(float d) {
+  static std::mutex mu;
+  static std::map<uint32_t, bool> cache;
+  uint32_t key;
+  std::memcpy(&key, &d, 4);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  unsigned int* flag = nullptr;
+  bool ok = false;
+  if (cudaMalloc(&flag, sizeof(unsigned int)) == cudaSuccess) {
+    cudaMemset(flag, 0, sizeof(unsigned int));
+    fk_verify_recip_div<<<148 * 16, 256>>>(d, flag);
+    unsigned int h = 1;
+    if (cudaMemcpy(&h, flag, sizeof h, cudaMemcpyDeviceToHost) == cudaSuccess) ok = h == 0;
+    cudaFree(flag);
+  }
+  cudaGetLastError();
+  std::lock_guard<std::mutex> lock(mu);
+  cache[key] = ok;
+  return ok;
 }
 
 int direct_elems() { return kD; }

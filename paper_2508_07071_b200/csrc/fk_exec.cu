@@ -462,9 +462,13 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
     }
     ok = ok && arith.size() <= 4 && uint32_t(p.write.in_kind) == (to_u8 ? FK_U8 : FK_F32);
     if (ok) {
-      uint32_t fn[4] = {0, 0, 0, 0};
-      for (size_t k = 0; k < arith.size(); ++k) fn[k] = arith[k].fn;
-      const uint32_t sig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], 0);
+      uint32_t fn[4] = {0, 0, 0, 0}, fast = 0;
+      for (size_t k = 0; k < arith.size(); ++k) {
+        fn[k] = arith[k].fn;
+        if (fn[k] == AF_DIV && recip_div_verified(f32_bits(arith[k].c[0]))) fast |= 1u << k;
+      }
+      uint32_t sig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast);
+      if (!direct_registered(sig)) sig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], 0);
       ok = direct_registered(sig);
       if (ok) {
         dp->direct_ok = true;

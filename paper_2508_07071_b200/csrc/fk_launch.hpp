@@ -21,6 +21,7 @@ int resample_elems();
 // compiled f32 element-wise chain kernel (fk_direct.cu)
 int direct_elems();
 bool direct_registered(uint32_t sig);
+bool recip_div_verified(float d);  // exhaustive 2^32-input device check, cached per divisor
 cudaError_t launch_direct(uint32_t sig, bool to_u8, const DPlan& P, cudaStream_t st);
 
 bool resample_affine_registered(uint32_t sig);  // fk_sig.cuh FK_AFFINE_SIGS

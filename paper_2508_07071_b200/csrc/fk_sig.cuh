@@ -33,6 +33,16 @@ __device__ __forceinline__ float div_by_recip(float x, float d, float r) {
   return __fmaf_rn(e, r, q);
 }
 
+// The same for any f32 input: normal-range magnitudes take the reciprocal form,
+// zeros / denormals / huge values / inf / NaN take IEEE division. Used for a
+// divisor only after fk_verify_recip_div has checked it against __fdiv_rn on all
+// 2^32 inputs (fk_direct.cu).
+__device__ __forceinline__ float div_guarded(float x, float d, float r) {
+  const float ax = fabsf(x);
+  if (ax >= 0x1p-100f && ax <= 0x1p100f) return div_by_recip(x, d, r);
+  return __fdiv_rn(x, d);
+}
+
 template <uint32_t SIG, int K>
 __device__ __forceinline__ float sig_op(float v, float c, float r) {
   constexpr uint32_t fn = sig_fn(SIG, K);
