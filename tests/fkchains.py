@@ -268,3 +268,41 @@ def reads_out_kind(spec: ChainSpec) -> int:
     for u in r.post:
         k = u[2] if u[0] == "cast" else (F32 if u[0] == "gray" else k)
     return k
+
+
+# ------------------------------------------------------------ serialisation --
+
+def spec_to_dict(spec: ChainSpec) -> dict:
+    """JSON-able description (sources are stored separately, by index)."""
+    return {"reads": [vars(r) | {"post": [list(u) for u in r.post]} for r in spec.reads],
+            "compute": [_ser(c) for c in spec.compute], "write_kind": spec.write_kind, "split": spec.split,
+            "batch": spec.batch, "active_read": spec.active_read, "active_write": spec.active_write,
+            "default": list(spec.default) if spec.default is not None else None,
+            "dst_stride_pad": spec.dst_stride_pad, "n_sources": len(spec.sources)}
+
+
+def _ser(c):
+    if c[0] == "loop":
+        return ["loop", _ser(c[1]), c[2]]
+    if c[0] == "batch_arith":
+        return ["batch_arith", c[1], c[2], [list(v) for v in c[3]]]
+    if c[0] == "arith":
+        return ["arith", c[1], c[2], list(c[3])]
+    return list(c)
+
+
+def _deser(c):
+    if c[0] == "loop":
+        return ("loop", _deser(c[1]), c[2])
+    if c[0] == "batch_arith":
+        return ("batch_arith", c[1], c[2], [tuple(v) for v in c[3]])
+    if c[0] == "arith":
+        return ("arith", c[1], c[2], tuple(c[3]))
+    return tuple(c)
+
+
+def spec_from_dict(d: dict, sources: list) -> ChainSpec:
+    reads = [ReadSpec(**(r | {"post": [tuple(u) for u in r["post"]]})) for r in d["reads"]]
+    return ChainSpec(sources, reads, [_deser(c) for c in d["compute"]], d["write_kind"], d["split"], d["batch"],
+                     d["active_read"], d["active_write"], tuple(d["default"]) if d["default"] is not None else None,
+                     d["dst_stride_pad"])
