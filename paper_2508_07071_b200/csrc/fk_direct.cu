@@ -63,11 +63,68 @@ __device__ __forceinline__ uint32_t f32_to_u8(float x) {
 
 }  // namespace
 
+template <bool TO_U8>
+__device__ __forceinline__ void load_tile(const DPlan& P, const DSample& s, uint32_t t, float (&v)[kD]) {
+  const uint32_t y = dev::fastdiv(t, P.tpr);
+  const uint32_t x = (t - y * P.tiles_per_row) * kD;
+  const int n = (P.width - x) < uint32_t(kD) ? int(P.width - x) : kD;
+  const uint8_t* p = reinterpret_cast<const uint8_t*>(s.src) + uint64_t(s.y0 + y) * s.pitch + uint64_t(s.x0 + x) * 4;
+  if (n == kD && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+#pragma unroll
+    for (int i = 0; i < kD / 4; ++i) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(p) + i);
+      v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+    }
+  } else {
+#pragma unroll
+    for (int e = 0; e < kD; ++e) v[e] = e < n ? __ldg(reinterpret_cast<const float*>(p) + e) : 0.f;
+  }
+}
+
+template <uint32_t SIG, bool TO_U8>
+__device__ __forceinline__ void finish_tile(const DPlan& P, const DWrite& w, uint32_t t, float (&v)[kD],
+                                            const float (&c)[4], const float (&r)[4], const uint32_t (&rep)[4]) {
+  const uint32_t y = dev::fastdiv(t, P.tpr);
+  const uint32_t x = (t - y * P.tiles_per_row) * kD;
+  const int n = (P.width - x) < uint32_t(kD) ? int(P.width - x) : kD;
+  const bool st = (w.flags & WF_STREAM) != 0;
+  direct_op<SIG, 0>(v, c[0], r[0], rep[0]);
+  direct_op<SIG, 1>(v, c[1], r[1], rep[1]);
+  direct_op<SIG, 2>(v, c[2], r[2], rep[2]);
+  direct_op<SIG, 3>(v, c[3], r[3], rep[3]);
+  uint8_t* q = reinterpret_cast<uint8_t*>(w.dst[0]) + uint64_t(y) * w.pitch[0];
+  if constexpr (TO_U8) {
+    uint32_t b[kD];
+#pragma unroll
+    for (int e = 0; e < kD; ++e) b[e] = f32_to_u8(v[e]);
+    q += x;
+    if (n == kD && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+      uint32_t wd[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        wd[i] = b[4 * i] | (b[4 * i + 1] << 8) | (b[4 * i + 2] << 16) | (b[4 * i + 3] << 24);
+      dev::store_words<4>(q, wd, st);
+    } else {
+      for (int e = 0; e < n; ++e) q[e] = uint8_t(b[e]);
+    }
+  } else {
+    q += uint64_t(x) * 4;
+    if (n == kD && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+      uint32_t wd[kD];
+#pragma unroll
+      for (int e = 0; e < kD; ++e) wd[e] = __float_as_uint(v[e]);
+      dev::store_words<kD>(q, wd, st);
+    } else {
+      for (int e = 0; e < n; ++e) reinterpret_cast<float*>(q)[e] = v[e];
+    }
+  }
+}
+
+// Grid-stride over the tiles of plane z with a machine-sized grid (no tail
+// wave), two tiles in flight per thread: both tiles' loads are issued before
+// either is computed, doubling the bytes in flight per SM.
 template <uint32_t SIG, bool TO_U8>
 __global__ void __launch_bounds__(kBlock) fk_direct(const __grid_constant__ DPlan P) {
-  const uint32_t t_begin = blockIdx.x * P.tiles_per_cta;
-  if (t_begin >= P.tiles) return;
-  const uint32_t t_end = min(t_begin + P.tiles_per_cta, P.tiles);
   float c[4] = {0.f, 0.f, 0.f, 0.f}, r[4] = {0.f, 0.f, 0.f, 0.f};
   uint32_t rep[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -79,58 +136,18 @@ __global__ void __launch_bounds__(kBlock) fk_direct(const __grid_constant__ DPla
       rep[k] = op.repeat;
     }
   }
+  const uint32_t stride = gridDim.x * kBlock;
   for (uint32_t z = blockIdx.z; z < P.batch; z += gridDim.z) {
     const DSample s = P.reads[z];
     const DWrite w = P.writes[z];
     if (!(w.flags & WF_ACTIVE)) continue;
-    const bool st = (w.flags & WF_STREAM) != 0;
-    for (uint32_t t = t_begin + threadIdx.x; t < t_end; t += kBlock) {
-      const uint32_t y = dev::fastdiv(t, P.tpr);
-      const uint32_t x = (t - y * P.tiles_per_row) * kD;
-      const int n = (P.width - x) < uint32_t(kD) ? int(P.width - x) : kD;
-      const uint8_t* p = reinterpret_cast<const uint8_t*>(s.src) + uint64_t(s.y0 + y) * s.pitch +
-                         uint64_t(s.x0 + x) * 4;
-      float v[kD];
-      if (n == kD && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
-#pragma unroll
-        for (int i = 0; i < kD / 4; ++i) {
-          const float4 q = __ldg(reinterpret_cast<const float4*>(p) + i);
-          v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < kD; ++e) v[e] = e < n ? __ldg(reinterpret_cast<const float*>(p) + e) : 0.f;
-      }
-      direct_op<SIG, 0>(v, c[0], r[0], rep[0]);
-      direct_op<SIG, 1>(v, c[1], r[1], rep[1]);
-      direct_op<SIG, 2>(v, c[2], r[2], rep[2]);
-      direct_op<SIG, 3>(v, c[3], r[3], rep[3]);
-      uint8_t* q = reinterpret_cast<uint8_t*>(w.dst[0]) + uint64_t(y) * w.pitch[0];
-      if constexpr (TO_U8) {
-        uint32_t b[kD];
-#pragma unroll
-        for (int e = 0; e < kD; ++e) b[e] = f32_to_u8(v[e]);
-        q += x;
-        if (n == kD && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
-          uint32_t wd[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            wd[i] = b[4 * i] | (b[4 * i + 1] << 8) | (b[4 * i + 2] << 16) | (b[4 * i + 3] << 24);
-          dev::store_words<4>(q, wd, st);
-        } else {
-          for (int e = 0; e < n; ++e) q[e] = uint8_t(b[e]);
-        }
-      } else {
-        q += uint64_t(x) * 4;
-        if (n == kD && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
-          uint32_t wd[kD];
-#pragma unroll
-          for (int e = 0; e < kD; ++e) wd[e] = __float_as_uint(v[e]);
-          dev::store_words<kD>(q, wd, st);
-        } else {
-          for (int e = 0; e < n; ++e) reinterpret_cast<float*>(q)[e] = v[e];
-        }
-      }
+    for (uint32_t t = blockIdx.x * kBlock + threadIdx.x; t < P.tiles; t += 2 * stride) {
+      const uint32_t t2 = t + stride;
+      float va[kD], vb[kD];
+      load_tile<TO_U8>(P, s, t, va);
+      if (t2 < P.tiles) load_tile<TO_U8>(P, s, t2, vb);
+      finish_tile<SIG, TO_U8>(P, w, t, va, c, r, rep);
+      if (t2 < P.tiles) finish_tile<SIG, TO_U8>(P, w, t2, vb, c, r, rep);
     }
   }
 }
@@ -183,14 +200,35 @@ bool direct_registered(uint32_t sig) {
   return false;
 }
 
+// CTAs per plane: enough to fill every SM at full occupancy (two tiles per thread), no more.
+template <class K>
+uint32_t direct_grid_x(K kernel, uint32_t tiles, uint32_t planes) {
+  static int resident = 0;  // CTAs per SM, queried once per instantiation
+  if (!resident) {
+    int dev = 0, sms = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kBlock, 0);
+    resident = (sms > 0 ? sms : 148) * (occ > 0 ? occ : 1);
+  }
+  const uint64_t want = (uint64_t(tiles) + 2 * kBlock - 1) / (2 * kBlock);
+  const uint64_t per_plane = (uint64_t(resident) + planes - 1) / planes;
+  return uint32_t(want < per_plane ? (want > 0 ? want : 1) : (per_plane > 0 ? per_plane : 1));
+}
+
 cudaError_t launch_direct(uint32_t sig, bool to_u8, const DPlan& P, cudaStream_t st) {
   if (P.tiles == 0 || P.batch == 0) return cudaSuccess;
-  const dim3 grid((P.tiles + P.tiles_per_cta - 1) / P.tiles_per_cta, 1, P.batch < 65535u ? P.batch : 65535u);
-#define FK_CASE(S)                                                          \
-  if (sig == (S)) {                                                         \
-    if (to_u8) fk_direct<S, true><<<grid, kBlock, 0, st>>>(P);              \
-    else fk_direct<S, false><<<grid, kBlock, 0, st>>>(P);                   \
-    return cudaGetLastError();                                              \
+  const uint32_t gz = P.batch < 65535u ? P.batch : 65535u;
+#define FK_CASE(S)                                                                            \
+  if (sig == (S)) {                                                                           \
+    if (to_u8) {                                                                              \
+      const dim3 grid(direct_grid_x(fk_direct<S, true>, P.tiles, gz), 1, gz);                 \
+      fk_direct<S, true><<<grid, kBlock, 0, st>>>(P);                                         \
+    } else {                                                                                  \
+      const dim3 grid(direct_grid_x(fk_direct<S, false>, P.tiles, gz), 1, gz);                \
+      fk_direct<S, false><<<grid, kBlock, 0, st>>>(P);                                        \
+    }                                                                                         \
+    return cudaGetLastError();                                                                \
   }
   FK_DIRECT_SIGS(FK_CASE)
 #undef FK_CASE
