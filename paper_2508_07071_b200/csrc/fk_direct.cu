@@ -63,66 +63,78 @@ __device__ __forceinline__ uint32_t f32_to_u8(float x) {
 
 }  // namespace
 
-template <bool TO_U8>
-__device__ __forceinline__ void load_tile(const DPlan& P, const DSample& s, uint32_t t, float (&v)[kD]) {
+// A warp tile is kWarpTile consecutive elements of one row; lane j owns the
+// four 4-element chunks at x0 + 128 i + 4 j (i = 0..3), so every warp-wide
+// 128-bit load or store covers 512 contiguous bytes (fully coalesced).
+constexpr uint32_t kWarpTile = 32 * kD;
+
+struct TileAt {
+  uint32_t y, x0;
+};
+__device__ __forceinline__ TileAt tile_at(const DPlan& P, uint32_t t) {
   const uint32_t y = dev::fastdiv(t, P.tpr);
-  const uint32_t x = (t - y * P.tiles_per_row) * kD;
-  const int n = (P.width - x) < uint32_t(kD) ? int(P.width - x) : kD;
-  const uint8_t* p = reinterpret_cast<const uint8_t*>(s.src) + uint64_t(s.y0 + y) * s.pitch + uint64_t(s.x0 + x) * 4;
-  if (n == kD && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+  return TileAt{y, (t - y * P.tiles_per_row) * kWarpTile};
+}
+
+__device__ __forceinline__ void load_tile(const DPlan& P, const DSample& s, TileAt at, uint32_t lane, float (&v)[kD]) {
+  const float* row = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(s.src) +
+                                                    uint64_t(s.y0 + at.y) * s.pitch) + s.x0;
 #pragma unroll
-    for (int i = 0; i < kD / 4; ++i) {
-      const float4 q = __ldg(reinterpret_cast<const float4*>(p) + i);
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t x = at.x0 + 128u * i + 4u * lane;
+    const float* p = row + x;
+    if (x + 4 <= P.width && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(p));
       v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
-    }
-  } else {
+    } else {
 #pragma unroll
-    for (int e = 0; e < kD; ++e) v[e] = e < n ? __ldg(reinterpret_cast<const float*>(p) + e) : 0.f;
+      for (int e = 0; e < 4; ++e) v[4 * i + e] = x + e < P.width ? __ldg(p + e) : 0.f;
+    }
   }
 }
 
 template <uint32_t SIG, bool TO_U8>
-__device__ __forceinline__ void finish_tile(const DPlan& P, const DWrite& w, uint32_t t, float (&v)[kD],
+__device__ __forceinline__ void finish_tile(const DPlan& P, const DWrite& w, TileAt at, uint32_t lane, float (&v)[kD],
                                             const float (&c)[4], const float (&r)[4], const uint32_t (&rep)[4]) {
-  const uint32_t y = dev::fastdiv(t, P.tpr);
-  const uint32_t x = (t - y * P.tiles_per_row) * kD;
-  const int n = (P.width - x) < uint32_t(kD) ? int(P.width - x) : kD;
   const bool st = (w.flags & WF_STREAM) != 0;
   direct_op<SIG, 0>(v, c[0], r[0], rep[0]);
   direct_op<SIG, 1>(v, c[1], r[1], rep[1]);
   direct_op<SIG, 2>(v, c[2], r[2], rep[2]);
   direct_op<SIG, 3>(v, c[3], r[3], rep[3]);
-  uint8_t* q = reinterpret_cast<uint8_t*>(w.dst[0]) + uint64_t(y) * w.pitch[0];
-  if constexpr (TO_U8) {
-    uint32_t b[kD];
+  uint8_t* row = reinterpret_cast<uint8_t*>(w.dst[0]) + uint64_t(at.y) * w.pitch[0];
 #pragma unroll
-    for (int e = 0; e < kD; ++e) b[e] = f32_to_u8(v[e]);
-    q += x;
-    if (n == kD && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
-      uint32_t wd[4];
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t x = at.x0 + 128u * i + 4u * lane;
+    if constexpr (TO_U8) {  // Cast f32 -> u8, then one 32-bit store per chunk
+      uint32_t b[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        wd[i] = b[4 * i] | (b[4 * i + 1] << 8) | (b[4 * i + 2] << 16) | (b[4 * i + 3] << 24);
-      dev::store_words<4>(q, wd, st);
+      for (int e = 0; e < 4; ++e) b[e] = f32_to_u8(v[4 * i + e]);
+      uint8_t* q = row + x;
+      if (x + 4 <= P.width && (reinterpret_cast<uintptr_t>(q) & 3) == 0) {
+        const uint32_t word = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
+        if (st) __stcs(reinterpret_cast<uint32_t*>(q), word);
+        else *reinterpret_cast<uint32_t*>(q) = word;
+      } else {
+        for (int e = 0; e < 4; ++e)
+          if (x + e < P.width) q[e] = uint8_t(b[e]);
+      }
     } else {
-      for (int e = 0; e < n; ++e) q[e] = uint8_t(b[e]);
-    }
-  } else {
-    q += uint64_t(x) * 4;
-    if (n == kD && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
-      uint32_t wd[kD];
-#pragma unroll
-      for (int e = 0; e < kD; ++e) wd[e] = __float_as_uint(v[e]);
-      dev::store_words<kD>(q, wd, st);
-    } else {
-      for (int e = 0; e < n; ++e) reinterpret_cast<float*>(q)[e] = v[e];
+      float* q = reinterpret_cast<float*>(row) + x;
+      if (x + 4 <= P.width && (reinterpret_cast<uintptr_t>(q) & 15) == 0) {
+        const float4 o = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        if (st) __stcs(reinterpret_cast<float4*>(q), o);
+        else *reinterpret_cast<float4*>(q) = o;
+      } else {
+        for (int e = 0; e < 4; ++e)
+          if (x + e < P.width) q[e] = v[4 * i + e];
+      }
     }
   }
 }
 
-// Grid-stride over the tiles of plane z with a machine-sized grid (no tail
-// wave), two tiles in flight per thread: both tiles' loads are issued before
-// either is computed, doubling the bytes in flight per SM.
+// Warps stride over the warp tiles of plane z with a machine-sized grid (no
+// tail wave); two tiles in flight per warp: both tiles' loads are issued before
+// either is computed.
 template <uint32_t SIG, bool TO_U8>
 __global__ void __launch_bounds__(kBlock) fk_direct(const __grid_constant__ DPlan P) {
   float c[4] = {0.f, 0.f, 0.f, 0.f}, r[4] = {0.f, 0.f, 0.f, 0.f};
@@ -136,18 +148,24 @@ __global__ void __launch_bounds__(kBlock) fk_direct(const __grid_constant__ DPla
       rep[k] = op.repeat;
     }
   }
-  const uint32_t stride = gridDim.x * kBlock;
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t warps = gridDim.x * (kBlock / 32);
   for (uint32_t z = blockIdx.z; z < P.batch; z += gridDim.z) {
     const DSample s = P.reads[z];
     const DWrite w = P.writes[z];
     if (!(w.flags & WF_ACTIVE)) continue;
-    for (uint32_t t = blockIdx.x * kBlock + threadIdx.x; t < P.tiles; t += 2 * stride) {
-      const uint32_t t2 = t + stride;
+    for (uint32_t t = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); t < P.tiles; t += 2 * warps) {
+      const uint32_t t2 = t + warps;
       float va[kD], vb[kD];
-      load_tile<TO_U8>(P, s, t, va);
-      if (t2 < P.tiles) load_tile<TO_U8>(P, s, t2, vb);
-      finish_tile<SIG, TO_U8>(P, w, t, va, c, r, rep);
-      if (t2 < P.tiles) finish_tile<SIG, TO_U8>(P, w, t2, vb, c, r, rep);
+      const TileAt a = tile_at(P, t);
+      load_tile(P, s, a, lane, va);
+      TileAt b{0, 0};
+      if (t2 < P.tiles) {
+        b = tile_at(P, t2);
+        load_tile(P, s, b, lane, vb);
+      }
+      finish_tile<SIG, TO_U8>(P, w, a, lane, va, c, r, rep);
+      if (t2 < P.tiles) finish_tile<SIG, TO_U8>(P, w, b, lane, vb, c, r, rep);
     }
   }
 }
@@ -191,7 +209,7 @@ bool recip_div_verified(float d) {
   return ok;
 }
 
-int direct_elems() { return kD; }
+int direct_elems() { return int(kWarpTile); }  // elements per (warp) tile
 
 bool direct_registered(uint32_t sig) {
 #define FK_CASE(S) if (sig == (S)) return true;
@@ -211,7 +229,7 @@ uint32_t direct_grid_x(K kernel, uint32_t tiles, uint32_t planes) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kBlock, 0);
     resident = (sms > 0 ? sms : 148) * (occ > 0 ? occ : 1);
   }
-  const uint64_t want = (uint64_t(tiles) + 2 * kBlock - 1) / (2 * kBlock);
+  const uint64_t want = (uint64_t(tiles) + 2 * (kBlock / 32) - 1) / (2 * (kBlock / 32));  // two warp tiles per warp
   const uint64_t per_plane = (uint64_t(resident) + planes - 1) / planes;
   return uint32_t(want < per_plane ? (want > 0 ? want : 1) : (per_plane > 0 ? per_plane : 1));
 }
