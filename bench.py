@@ -31,6 +31,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+from paper_2508_07071_b200.shard import shard_range, sum_over_ranks  # noqa: E402
+
 METRIC = "Mpixel/s and achieved HBM GB/s (% of 8 TB/s) per fused pipeline vs unfused and CPU"
 UNIT = "Mpixel/s"
 L2_FLUSH_BYTES = 512 << 20      # > 126 MB L2: written between timed steps
@@ -111,7 +113,9 @@ class ClockSampler:
 
 
 # --------------------------------------------------------------- workloads --
-def build(lib, workload: str, rank: int, crops: int, n_ops: int):
+def build(lib, workload: str, rank: int, crops: int, n_ops: int, world: int = 1, strong: bool = False):
+    """The workload's pipeline for this rank: weak scaling gives every rank `crops`
+    crops of its own; strong scaling splits `crops` into contiguous shards."""
     from paper_2508_07071_b200 import workloads as wl
     if workload == "c1":
         return wl.c1(lib)
@@ -120,8 +124,10 @@ def build(lib, workload: str, rank: int, crops: int, n_ops: int):
     if workload == "c3":
         return wl.c3(lib, n_ops)
     if workload == "c4":
-        return wl.crops_224(lib, crops, per_crop_norm=True, name="C4", first=rank * crops)
-    return wl.crops_224(lib, crops, per_crop_norm=False, name="C5", first=rank * crops)
+        lo, hi = shard_range(crops, rank, world) if strong else (rank * crops, (rank + 1) * crops)
+        return wl.crops_224(lib, hi - lo, per_crop_norm=True, name="C4", first=lo)
+    lo, hi = shard_range(crops, rank, world) if strong else (rank * crops, (rank + 1) * crops)
+    return wl.crops_224(lib, hi - lo, per_crop_norm=False, name="C5", first=lo)
 
 
 def describe(w, workload, crops, n_ops, world):
@@ -182,7 +188,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="c5", choices=["c1", "c2", "c3", "c4", "c5"])
     ap.add_argument("--impl", default="fk", choices=["fk", "reference"])
-    ap.add_argument("--crops", type=int, default=8192)
+    ap.add_argument("--crops", type=int, default=8192, help="crops per GPU (weak) or in total (strong)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"])
     ap.add_argument("--n-ops", type=int, default=64)
     ap.add_argument("--cpu-sample-crops", type=int, default=256)
     ap.add_argument("--cpu-budget-s", type=float, default=10.0)
@@ -218,7 +225,8 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     lib = Library("cuda")
-    w = build(lib, args.workload, rank, args.crops, args.n_ops)
+    w = build(lib, args.workload, rank, args.crops, args.n_ops, world, args.scaling == "strong")
+    job_points = sum_over_ranks(w.points, "cuda") if world > 1 else w.points
     stream = torch.cuda.current_stream()
     cfg = ExecConfig(stream=stream.cuda_stream, force_generic=args.force_generic)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device="cuda")
@@ -255,7 +263,7 @@ def main():
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
-    value = world * w.points * args.steps / (total_ms / 1e3) / 1e6
+    value = job_points * args.steps / (total_ms / 1e3) / 1e6
 
     # ---- unfused comparator (same workload, one launch per op)
     unfused = None
@@ -302,7 +310,7 @@ def main():
             t = torch.tensor([ems], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
-        e2e = {"value": world * w.points / (ems / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
+        e2e = {"value": job_points / (ems / 1e3) / 1e6, "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "ms_per_step": ems}
 
     if world > 1:
@@ -324,7 +332,7 @@ def main():
         cpu, _ = run_reference(args, args.workload, args.cpu_sample_crops, args.cpu_budget_s)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": describe(w, args.workload, args.crops, args.n_ops, world),
             "gbs": achieved, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "unfused": unfused,
