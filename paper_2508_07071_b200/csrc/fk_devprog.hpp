@@ -88,6 +88,8 @@ struct DPlan {
   uint32_t prog_swap;        // compute program swaps lanes 0/2 an odd number of times
   const DOp* table;          // [compute ops..., folded-unary programs...] in HBM (long programs)
   DOp prog[kProg];           // same layout, inline
+  const uint32_t* order;     // visiting order of the planes (blockIdx.z -> z), nullptr = identity:
+                             // planes sharing a source are adjacent so it stays L2-resident
   const DSample* reads;      // batch entries; nullptr -> affine read below
   const DWrite* writes;      // batch entries; nullptr -> affine write below
   DSample rd;                // affine read: plane z at rd.src + z * rd_zstride

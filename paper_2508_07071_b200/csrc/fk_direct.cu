@@ -46,10 +46,32 @@ __device__ __forceinline__ float direct_elem(float v, float c, float r) {
 template <uint32_t SIG, int K>
 __device__ __forceinline__ void direct_op(float (&v)[kD], float c, float r, uint32_t reps) {
   if constexpr (K < sig_n(SIG)) {
+    if constexpr (sig_fn(SIG, K) == AF_DIV && sig_fast(SIG, K)) {
+      // div_guarded for the whole tile: reciprocal form everywhere, then (rarely)
+      // IEEE division for the elements outside its verified range
 #pragma unroll 1
-    for (uint32_t i = 0; i < reps; ++i)
+      for (uint32_t i = 0; i < reps; ++i) {
+        float q[kD];
+        bool all = true;
 #pragma unroll
-      for (int e = 0; e < kD; ++e) v[e] = direct_elem<SIG, K>(v[e], c, r);
+        for (int e = 0; e < kD; ++e) {
+          q[e] = div_by_recip(v[e], c, r);
+          all = all && recip_range(v[e]);
+        }
+        if (!all) {
+#pragma unroll
+          for (int e = 0; e < kD; ++e)
+            if (!recip_range(v[e])) q[e] = __fdiv_rn(v[e], c);
+        }
+#pragma unroll
+        for (int e = 0; e < kD; ++e) v[e] = q[e];
+      }
+    } else {
+#pragma unroll 1
+      for (uint32_t i = 0; i < reps; ++i)
+#pragma unroll
+        for (int e = 0; e < kD; ++e) v[e] = direct_elem<SIG, K>(v[e], c, r);
+    }
   }
 }
 
@@ -150,7 +172,8 @@ __global__ void __launch_bounds__(kBlock) fk_direct(const __grid_constant__ DPla
   }
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warps = gridDim.x * (kBlock / 32);
-  for (uint32_t z = blockIdx.z; z < P.batch; z += gridDim.z) {
+  for (uint32_t zi = blockIdx.z; zi < P.batch; zi += gridDim.z) {
+    const uint32_t z = P.order ? __ldg(P.order + zi) : zi;
     const DSample s = P.reads[z];
     const DWrite w = P.writes[z];
     if (!(w.flags & WF_ACTIVE)) continue;

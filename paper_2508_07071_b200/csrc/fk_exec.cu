@@ -7,6 +7,7 @@
 // Counters follow the reference's accounting exactly (fk_core.cpp:analytic_traffic).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -174,6 +175,7 @@ struct DeviceProgram {
   std::map<uint64_t, std::vector<uint64_t>> per_z_host;  // BatchArith rows by device address
   DSample* d_reads = nullptr;
   DWrite* d_writes = nullptr;
+  uint32_t* d_order = nullptr;   // plane visiting order (grouped by source), or null
   std::vector<void*> extra;      // BatchArith constant tables
   std::vector<DSample> reads;    // host copies
   bool read_flat = false, write_flat = false;
@@ -186,7 +188,8 @@ struct DeviceProgram {
   Traffic traffic;               // analytic ExecReport counters (computed once)
 
   ~DeviceProgram() {
-    for (void* p : {static_cast<void*>(d_table), static_cast<void*>(d_reads), static_cast<void*>(d_writes)})
+    for (void* p : {static_cast<void*>(d_table), static_cast<void*>(d_reads), static_cast<void*>(d_writes),
+                    static_cast<void*>(d_order)})
       if (p) cudaFree(p);
     for (void* p : extra) cudaFree(p);
   }
@@ -479,6 +482,23 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
       }
     }
   }
+  // Visit planes grouped by source buffer (then by crop origin): the crops of one
+  // frame run back to back, so the frame stays L2-resident instead of every
+  // frame of the batch competing for L2 at once. Any order is correct: planes
+  // are independent (ops.cpp:369-378).
+  if (B > 1) {
+    std::vector<uint32_t> order(B);
+    for (uint32_t z = 0; z < B; ++z) order[z] = z;
+    std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+      const DSample &x = dp->reads[a], &y = dp->reads[b];
+      if (x.src != y.src) return x.src < y.src;
+      if (x.y0 != y.y0) return x.y0 < y.y0;
+      return x.x0 < y.x0;
+    });
+    bool identity = true;
+    for (uint32_t z = 0; z < B; ++z) identity = identity && order[z] == z;
+    if (!identity) dp->d_order = upload(order);
+  }
   dp->traffic = analytic_traffic(p);
   dp->d_table = upload(dp->table);
   dp->d_reads = upload(dp->reads);
@@ -576,6 +596,7 @@ uint64_t now_ns() {
 
 void fill_plan_io(DPlan& P, const DeviceProgram& dp, const Pipeline& p, const fk_exec_config* cfg) {
   P.table = dp.d_table;
+  P.order = dp.d_order;
   P.prog_inline = dp.table.size() <= kProg ? 1u : 0u;
   if (P.prog_inline) std::memcpy(P.prog, dp.table.data(), dp.table.size() * sizeof(DOp));
   P.def_kind = dp.def_kind;

@@ -29,7 +29,8 @@ __global__ void __launch_bounds__(kBlock, FK_MIN_BLOCKS) fk_transform_generic(co
   const uint32_t t_end = min(t_begin + P.tiles_per_cta, P.tiles);
   const uint32_t y_first = dev::fastdiv(t_begin, P.tpr);
   const uint32_t rows = dev::fastdiv(t_end - 1, P.tpr) - y_first + 1;
-  for (uint32_t z = blockIdx.z; z < P.batch; z += gridDim.z) {
+  for (uint32_t zi = blockIdx.z; zi < P.batch; zi += gridDim.z) {
+    const uint32_t z = P.order ? __ldg(P.order + zi) : zi;
     DSample s;
     if (P.reads) {
       s = P.reads[z];

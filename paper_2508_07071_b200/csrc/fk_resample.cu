@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(kBlock, 3) fk_resample(const __grid_constant__
   const uint32_t y_first = dev::fastdiv(t_begin, P.tpr);
   const uint32_t rows = dev::fastdiv(t_end - 1, P.tpr) - y_first + 1;
   const bool tab = P.width <= kXCap && rows <= kYCap;
-  for (uint32_t z = blockIdx.z; z < P.batch; z += gridDim.z) {
+  for (uint32_t zi = blockIdx.z; zi < P.batch; zi += gridDim.z) {
+    const uint32_t z = P.order ? __ldg(P.order + zi) : zi;
     const DSample s = P.reads[z];
     const DWrite w = P.writes[z];
     const bool swap = ((s.flags & SF_POST_SWAP) != 0) != (P.prog_swap != 0);

@@ -37,10 +37,12 @@ __device__ __forceinline__ float div_by_recip(float x, float d, float r) {
 // zeros / denormals / huge values / inf / NaN take IEEE division. Used for a
 // divisor only after fk_verify_recip_div has checked it against __fdiv_rn on all
 // 2^32 inputs (fk_direct.cu).
+// |x| in [2^-100, 2^100) as one integer compare on the bit pattern (NaN/inf/0/denormal fail).
+__device__ __forceinline__ bool recip_range(float x) {
+  return ((__float_as_uint(x) & 0x7fffffffu) - 0x0d800000u) < 0x64000000u;
+}
 __device__ __forceinline__ float div_guarded(float x, float d, float r) {
-  const float ax = fabsf(x);
-  if (ax >= 0x1p-100f && ax <= 0x1p100f) return div_by_recip(x, d, r);
-  return __fdiv_rn(x, d);
+  return recip_range(x) ? div_by_recip(x, d, r) : __fdiv_rn(x, d);
 }
 
 template <uint32_t SIG, int K>
