@@ -610,6 +610,16 @@ void fill_plan_io(DPlan& P, const DeviceProgram& dp, const Pipeline& p, const fk
 
 bool lut_allowed(const fk_exec_config* cfg) { return !(cfg && (cfg->flags & FK_EXEC_NO_LUT)); }
 
+// FK_RESAMPLE_TILES=1 selects the earlier tile-per-thread resample kernel
+// (fk_resample.cu) instead of the column-streaming one, for A/B profiling.
+bool tile_resample() {
+  static const bool on = [] {
+    const char* e = std::getenv("FK_RESAMPLE_TILES");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 }  // namespace
 
 void check_config(const fk_exec_config* c) {  // executor.cpp:20-25
@@ -645,6 +655,24 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
   P.writes = dp.d_writes;
   if (direct) {
     cuda_check(launch_direct(dp.dir_sig, dp.direct_u8, P, st), "fk_direct launch");
+    ++r.kernels_launched;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    r.path = FK_PATH_COMPILED;
+  } else if (compiled && !tile_resample()) {
+    // column-streaming kernel: 2D grid (column strips x row bands x planes)
+    const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
+    const uint32_t block = std::min<uint32_t>(256, (W + 31) / 32 * 32);
+    const uint64_t strips = (W + block - 1) / block;
+    const uint64_t work = uint64_t(H) * strips * B;
+    uint64_t band = work / (148ull * 12);
+    band = std::max<uint64_t>(4, std::min<uint64_t>(resample_sep_band_max(), band));
+    DPlan S = P;
+    S.width = W;
+    S.height = H;
+    S.tiles_per_cta = uint32_t(band);
+    cuda_check(launch_resample_sep(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)), P.write_mode == WR_SPLIT,
+                                   affine ? dp.aff_sig : kSigLut, S, block, st),
+               "fk_resample_sep launch");
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     r.path = FK_PATH_COMPILED;

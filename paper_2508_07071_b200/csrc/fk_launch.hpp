@@ -24,6 +24,11 @@ bool direct_registered(uint32_t sig);
 bool recip_div_verified(float d);  // exhaustive 2^32-input device check, cached per divisor
 cudaError_t launch_direct(uint32_t sig, bool to_u8, const DPlan& P, cudaStream_t st);
 
+// compiled column-streaming u8 resample kernel (fk_resample_sep.cu); P.tiles_per_cta = band rows
+uint32_t resample_sep_band_max();
+cudaError_t launch_resample_sep(int src_lanes, uint32_t out_lane_kind, bool split, uint32_t sig, const DPlan& P,
+                                uint32_t block, cudaStream_t st);
+
 bool resample_affine_registered(uint32_t sig);  // fk_sig.cuh FK_AFFINE_SIGS
 // sig == kSigLut: LUT mode; else the registered AFFINE chain signature
 cudaError_t launch_resample(int src_lanes, uint32_t out_lane_kind, bool split, uint32_t sig, const DPlan& P,
