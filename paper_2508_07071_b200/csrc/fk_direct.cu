@@ -51,20 +51,16 @@ __device__ __forceinline__ void direct_op(float (&v)[kD], float c, float r, uint
       // IEEE division for the elements outside its verified range
 #pragma unroll 1
       for (uint32_t i = 0; i < reps; ++i) {
-        float q[kD];
         bool all = true;
 #pragma unroll
-        for (int e = 0; e < kD; ++e) {
-          q[e] = div_by_recip(v[e], c, r);
-          all = all && recip_range(v[e]);
-        }
-        if (!all) {
+        for (int e = 0; e < kD; ++e) all = all && recip_range(v[e]);
+        if (all) {
 #pragma unroll
-          for (int e = 0; e < kD; ++e)
-            if (!recip_range(v[e])) q[e] = __fdiv_rn(v[e], c);
-        }
+          for (int e = 0; e < kD; ++e) v[e] = div_by_recip(v[e], c, r);
+        } else {
 #pragma unroll
-        for (int e = 0; e < kD; ++e) v[e] = q[e];
+          for (int e = 0; e < kD; ++e) v[e] = div_guarded(v[e], c, r);
+        }
       }
     } else {
 #pragma unroll 1
@@ -158,7 +154,7 @@ __device__ __forceinline__ void finish_tile(const DPlan& P, const DWrite& w, Til
 // tail wave); two tiles in flight per warp: both tiles' loads are issued before
 // either is computed.
 template <uint32_t SIG, bool TO_U8>
-__global__ void __launch_bounds__(kBlock) fk_direct(const __grid_constant__ DPlan P) {
+__global__ void __launch_bounds__(kBlock, 3) fk_direct(const __grid_constant__ DPlan P) {
   float c[4] = {0.f, 0.f, 0.f, 0.f}, r[4] = {0.f, 0.f, 0.f, 0.f};
   uint32_t rep[4] = {0, 0, 0, 0};
 #pragma unroll

@@ -9,15 +9,15 @@
 // and `top`/`bot` depend only on (source row, output column). So each thread
 // owns ONE output column and walks down a band of output rows, holding the
 // horizontal lerps of the two current source rows in registers: a source row's
-// H-lerp is computed once however many output rows use it, the V-lerp is the
-// only per-pixel double work. Same double ops, same order: bit-exact.
+// H-lerp is computed once however many output rows use it, and the V-lerp is
+// the only per-pixel double work. Same double ops in the same order: bit-exact.
 //
 //   CTA = a strip of up to 256 consecutive output columns x a band of rows of
 //   one plane z (blockIdx.z, horizontal fusion). Per CTA and plane: the rows'
 //   coordinates in shared memory, the chain's constants in registers (AFFINE:
 //   Cast u8->f32 + a registered f32 chain) or its 256-entry table (LUT: any
-//   lane-wise chain). Nearest and non-resizing planes take the same path with
-//   one tap.
+//   lane-wise chain). The plane's mode (bilinear / one tap) and whether its rows
+//   are 4-byte aligned are resolved once per CTA into specialised loop bodies.
 #include <cuda_runtime.h>
 
 #include <type_traits>
@@ -32,34 +32,175 @@ namespace {
 
 constexpr uint32_t kBandMax = 64;  // output rows per CTA (host picks <= this)
 
-// u8 lanes of the two taps of one source row (bytes at row + o0 and row + o1).
+struct RowEnt {                    // one output row: source rows (absolute) and fy
+  uint32_t s0, s1;
+  double f;
+};
+
+// Per-column gather geometry for 4-byte-aligned source rows: the taps' bytes
+// [o0, o1 + 3) lie in words w[0..2] from (row + (o0 & ~3)); a word is loaded only
+// if it holds one of those bytes (so nothing past the plane is touched).
+struct ColGeom {
+  uint32_t woff;         // byte offset of the first word within the row
+  uint32_t sa, sb;       // funnel-shift amounts of tap 0 / tap 1 (bits)
+  uint32_t need1, need2; // load word 1 / word 2
+};
+
+__device__ __forceinline__ ColGeom col_geom(uint32_t o0, uint32_t o1) {
+  const uint32_t r = o0 & 3u, last = r + (o1 - o0) + 2;
+  return ColGeom{o0 & ~3u, 8 * r, 8 * (r + (o1 - o0)), last >= 4 ? 1u : 0u, last >= 8 ? 1u : 0u};
+}
+
+__device__ __forceinline__ uint32_t ld_if(const uint32_t* p, uint32_t need) {
+  uint32_t v = 0;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
+               : "+r"(v) : "l"(p), "r"(need));
+  return v;
+}
+
+// the two 3-byte taps of one source row (aligned-row fast path)
+__device__ __forceinline__ void taps_aligned(const uint8_t* row, const ColGeom& g, uint32_t& a, uint32_t& b) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(row + g.woff);
+  const uint32_t w0 = __ldg(w), w1 = ld_if(w + 1, g.need1), w2 = ld_if(w + 2, g.need2);
+  a = __funnelshift_r(w0, w1, g.sa);
+  b = g.sb < 32 ? __funnelshift_r(w0, w1, g.sb) : __funnelshift_r(w1, w2, g.sb - 32);
+}
+
+// byte l of v as a double: 2^52 + v is exact and its low word is v
+__device__ __forceinline__ double byte_as_biased_double(uint32_t v, int l) {
+  return __hiloint2double(0x43300000, int(__byte_perm(v, 0, 0x4440 | l)));
+}
+
+// Horizontal lerp a + (b - a) * fx of one source row, per lane (ops.cpp:283-284).
 template <int NL>
-__device__ __forceinline__ void taps_u8(const uint8_t* row, uint32_t o0, uint32_t o1, uint32_t& a, uint32_t& b) {
+__device__ __forceinline__ void hlerp(uint32_t a, uint32_t b, double fx, double (&h)[3]) {
+  constexpr double kTwo52 = 4503599627370496.0;
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    const double A = byte_as_biased_double(a, l), B = byte_as_biased_double(b, l);
+    h[l] = __dadd_rn(__dsub_rn(A, kTwo52), __dmul_rn(__dsub_rn(B, A), fx));
+  }
+}
+
+template <int NL, bool ALIGNED>
+__device__ __forceinline__ void row_taps(const uint8_t* row, const ColGeom& g, uint32_t o0, uint32_t o1,
+                                         uint32_t& a, uint32_t& b) {
   if constexpr (NL == 3) {
-    dev::load_u8x3_taps(row, o0, o1, a, b);
+    if constexpr (ALIGNED) taps_aligned(row, g, a, b);
+    else dev::load_u8x3_taps(row, o0, o1, a, b);
   } else {
     a = __ldg(row + o0);
     b = __ldg(row + o1);
   }
 }
 
-// Horizontal lerp of one source row for this column: a + (b - a) * fx in
-// double per lane (ops.cpp:283-284), with 2^52 + v as the exact int->double.
-template <int NL>
-__device__ __forceinline__ void hlerp(const uint8_t* row, uint32_t o0, uint32_t o1, double fx, bool lerp,
-                                      double (&h)[3]) {
-  uint32_t a, b;
-  taps_u8<NL>(row, o0, o1, a, b);
-  constexpr double kTwo52 = 4503599627370496.0;
+// The chain after the u8 read, on the lanes of one output pixel.
+template <int NL, uint32_t OLK, uint32_t SIG, class Out>
+__device__ __forceinline__ void chain(uint32_t (&u)[3], bool swap, const float (&acst)[4][3], const float (&arcp)[4][3],
+                                      const Out (*lut)[256], Out (&o)[NL]) {
+  if constexpr (NL == 3) {
+    if (swap) { const uint32_t t = u[0]; u[0] = u[2]; u[2] = t; }
+  }
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
-    const double A = __hiloint2double(0x43300000, int((a >> (8 * l)) & 0xffu));
-    if (lerp) {
-      const double B = __hiloint2double(0x43300000, int((b >> (8 * l)) & 0xffu));
-      h[l] = __dadd_rn(__dsub_rn(A, kTwo52), __dmul_rn(__dsub_rn(B, A), fx));
+    if constexpr (SIG != kSigLut) {
+      float c[4], r[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        c[k] = k < sig_n(SIG) ? acst[k][l] : 0.f;
+        r[k] = k < sig_n(SIG) ? arcp[k][l] : 0.f;
+      }
+      o[l] = Out(__float_as_uint(sig_apply<SIG>(float(u[l]), c, r)));  // Cast u8 -> f32, chain
     } else {
-      h[l] = __dsub_rn(A, kTwo52);  // nearest / direct: the tap itself
+      o[l] = lut[l][u[l]];
     }
+  }
+}
+
+template <int NL, uint32_t OLK, bool SPLIT, class Out>
+__device__ __forceinline__ void store_px(const DWrite& w, uint32_t x, uint32_t y, const Out (&o)[NL], bool al) {
+  constexpr int OB = OLK == FK_U8 ? 1 : (OLK == FK_F32 ? 4 : 8);
+  if constexpr (SPLIT) {  // split_block, ops.cpp:402-424
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      uint8_t* p = reinterpret_cast<uint8_t*>(w.dst[l]) + uint64_t(y) * w.pitch[l] + uint64_t(x) * OB;
+      if constexpr (OLK == FK_F32) {
+        if (al) {
+          __stcs(reinterpret_cast<float*>(p), __uint_as_float(uint32_t(o[l])));
+          continue;
+        }
+      }
+      dev::store_lane<OLK, Out>(p, o[l], al);
+    }
+  } else {  // store_block, ops.cpp:396-400
+    uint8_t* p = reinterpret_cast<uint8_t*>(w.dst[0]) + uint64_t(y) * w.pitch[0] + uint64_t(x) * OB * NL;
+#pragma unroll
+    for (int l = 0; l < NL; ++l) dev::store_lane<OLK, Out>(p + l * OB, o[l], al);
+  }
+}
+
+// Walk output rows [y0, y1) of column x: bilinear, source rows 4-byte aligned or not.
+template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool ALIGNED, class Out>
+__device__ __forceinline__ void column_bilinear(const DSample& s, const DWrite& w, const RowEnt* rows, uint32_t x,
+                                                uint32_t y0, uint32_t y1, bool swap, const float (&acst)[4][3],
+                                                const float (&arcp)[4][3], const Out (*lut)[256], bool al) {
+  const XEnt xe = dev::x_entry(s, x, NL);
+  const ColGeom g = col_geom(xe.o0, xe.o1);
+  const uint8_t* base = reinterpret_cast<const uint8_t*>(s.src);
+  uint32_t held0 = 0xffffffffu, held1 = 0xffffffffu;  // source rows whose H-lerps h0 / h1 hold
+  double h0[3] = {0, 0, 0}, h1[3] = {0, 0, 0};
+  for (uint32_t y = y0; y < y1; ++y) {
+    const RowEnt re = rows[y - y0];
+    // rows only move down: the new top row is the held top, the held bottom, or new
+    if (re.s0 != held0) {
+      if (re.s0 == held1) {
+#pragma unroll
+        for (int l = 0; l < 3; ++l) h0[l] = h1[l];
+      } else {
+        uint32_t a, b;
+        row_taps<NL, ALIGNED>(base + uint64_t(re.s0) * s.pitch, g, xe.o0, xe.o1, a, b);
+        hlerp<NL>(a, b, xe.f, h0);
+      }
+      held0 = re.s0;
+    }
+    if (re.s1 != held1) {
+      if (re.s1 == re.s0) {
+#pragma unroll
+        for (int l = 0; l < 3; ++l) h1[l] = h0[l];
+      } else {
+        uint32_t a, b;
+        row_taps<NL, ALIGNED>(base + uint64_t(re.s1) * s.pitch, g, xe.o0, xe.o1, a, b);
+        hlerp<NL>(a, b, xe.f, h1);
+      }
+      held1 = re.s1;
+    }
+    uint32_t u[3];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) {  // top + (bot - top) * fy, round_clamp_u8 (res in [0, 255])
+      const double res = __dadd_rn(h0[l], __dmul_rn(__dsub_rn(h1[l], h0[l]), re.f));
+      u[l] = uint32_t(__double2loint(__dadd_rn(res, 6755399441055744.0)));
+    }
+    Out o[NL];
+    chain<NL, OLK, SIG, Out>(u, swap, acst, arcp, lut, o);
+    store_px<NL, OLK, SPLIT, Out>(w, x, y, o, al);
+  }
+}
+
+// Nearest / non-resizing planes: one tap per output pixel.
+template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, class Out>
+__device__ __forceinline__ void column_tap(const DSample& s, const DWrite& w, const RowEnt* rows, uint32_t x,
+                                           uint32_t y0, uint32_t y1, bool swap, const float (&acst)[4][3],
+                                           const float (&arcp)[4][3], const Out (*lut)[256], bool al) {
+  const uint32_t o0 = s.mode == RD_DIRECT ? (s.x0 + x) * NL : dev::x_entry(s, x, NL).o0;
+  const uint8_t* base = reinterpret_cast<const uint8_t*>(s.src) + o0;
+  for (uint32_t y = y0; y < y1; ++y) {
+    const uint8_t* p = base + uint64_t(rows[y - y0].s0) * s.pitch;
+    uint32_t u[3];
+#pragma unroll
+    for (int l = 0; l < NL; ++l) u[l] = __ldg(p + l);
+    Out o[NL];
+    chain<NL, OLK, SIG, Out>(u, swap, acst, arcp, lut, o);
+    store_px<NL, OLK, SPLIT, Out>(w, x, y, o, al);
   }
 }
 
@@ -69,8 +210,7 @@ template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG>
 __global__ void __launch_bounds__(256) fk_resample_sep(const __grid_constant__ DPlan P) {
   constexpr bool AFFINE = SIG != kSigLut;
   using Out = typename std::conditional<OLK == FK_F64, uint64_t, uint32_t>::type;
-  constexpr int OB = OLK == FK_U8 ? 1 : (OLK == FK_F32 ? 4 : 8);
-  __shared__ YEnt yt[kBandMax];
+  __shared__ RowEnt rows[kBandMax];
   __shared__ Out lut[AFFINE ? 1 : NL][AFFINE ? 1 : 256];
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t y_begin = blockIdx.y * P.tiles_per_cta;  // tiles_per_cta = band rows for this kernel
@@ -80,8 +220,6 @@ __global__ void __launch_bounds__(256) fk_resample_sep(const __grid_constant__ D
     const DSample s = P.reads[z];
     const DWrite w = P.writes[z];
     const bool swap = ((s.flags & SF_POST_SWAP) != 0) != (P.prog_swap != 0);
-    const bool resampling = s.mode != RD_DIRECT;
-    const bool bilinear = s.mode == RD_BILINEAR;
     float acst[4][3], arcp[4][3];
     if constexpr (AFFINE) {
 #pragma unroll
@@ -101,14 +239,17 @@ __global__ void __launch_bounds__(256) fk_resample_sep(const __grid_constant__ D
     }
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < y_end - y_begin; j += blockDim.x) {
-      if (resampling) {
-        yt[j] = dev::y_entry(s, y_begin + j);
+      RowEnt e;
+      if (s.mode != RD_DIRECT) {  // y_entry gives row byte offsets; keep the source row numbers
+        const YEnt ye = dev::y_entry(s, y_begin + j);
+        e.s0 = uint32_t(ye.r0 / s.pitch);
+        e.s1 = uint32_t(ye.r1 / s.pitch);
+        e.f = ye.f;
       } else {
-        YEnt e;
-        e.r0 = e.r1 = uint64_t(s.y0 + y_begin + j) * s.pitch;
+        e.s0 = e.s1 = s.y0 + y_begin + j;
         e.f = 0.0;
-        yt[j] = e;
       }
+      rows[j] = e;
     }
     if constexpr (!AFFINE) {
       for (uint32_t t = threadIdx.x; t < 256; t += blockDim.x) {  // the chain over every byte value
@@ -121,100 +262,15 @@ __global__ void __launch_bounds__(256) fk_resample_sep(const __grid_constant__ D
     }
     __syncthreads();
     if (!(w.flags & WF_ACTIVE) || x >= P.width) continue;  // BatchWrite z >= active_count / past the row
-    // this column's taps
-    uint32_t o0, o1;
-    double fx = 0.0;
-    if (resampling) {
-      const XEnt xe = dev::x_entry(s, x, NL);
-      o0 = xe.o0;
-      o1 = xe.o1;
-      fx = xe.f;
+    const bool al = (w.flags & WF_LANE_ALIGNED) != 0;
+    const bool aligned_rows = ((s.src | s.pitch) & 3) == 0;
+    if (s.mode == RD_BILINEAR) {
+      if (aligned_rows)
+        column_bilinear<NL, OLK, SPLIT, SIG, true, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut, al);
+      else
+        column_bilinear<NL, OLK, SPLIT, SIG, false, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut, al);
     } else {
-      o0 = o1 = (s.x0 + x) * NL;
-    }
-    const uint8_t* base = reinterpret_cast<const uint8_t*>(s.src);
-    const bool st = (w.flags & WF_STREAM) != 0;
-    // horizontal lerps of the source rows used by the previous output row
-    uint64_t held0 = ~uint64_t(0), held1 = ~uint64_t(0);
-    double h0[3] = {0, 0, 0}, h1[3] = {0, 0, 0};
-    for (uint32_t y = y_begin; y < y_end; ++y) {
-      const YEnt ye = yt[y - y_begin];
-      // rows advance monotonically: reuse a held row, else compute its H-lerp once
-      double n0[3], n1[3];
-      if (ye.r0 == held0) {
-#pragma unroll
-        for (int l = 0; l < 3; ++l) n0[l] = h0[l];
-      } else if (ye.r0 == held1) {
-#pragma unroll
-        for (int l = 0; l < 3; ++l) n0[l] = h1[l];
-      } else {
-        hlerp<NL>(base + ye.r0, o0, o1, fx, bilinear, n0);
-      }
-      if (bilinear) {
-        if (ye.r1 == ye.r0) {
-#pragma unroll
-          for (int l = 0; l < 3; ++l) n1[l] = n0[l];
-        } else if (ye.r1 == held1) {
-#pragma unroll
-          for (int l = 0; l < 3; ++l) n1[l] = h1[l];
-        } else {
-          hlerp<NL>(base + ye.r1, o0, o1, fx, true, n1);
-        }
-      }
-      held0 = ye.r0;
-      held1 = bilinear ? ye.r1 : ye.r0;
-      uint32_t u[3];
-#pragma unroll
-      for (int l = 0; l < 3; ++l) {
-        h0[l] = n0[l];
-        h1[l] = bilinear ? n1[l] : n0[l];
-      }
-#pragma unroll
-      for (int l = 0; l < NL; ++l) {
-        if (bilinear) {  // top + (bot - top) * fy, then round_clamp_u8 (res is in [0, 255])
-          const double res = __dadd_rn(h0[l], __dmul_rn(__dsub_rn(h1[l], h0[l]), ye.f));
-          u[l] = uint32_t(__double2loint(__dadd_rn(res, 6755399441055744.0)));
-        } else {
-          u[l] = uint32_t(__double2loint(__dadd_rn(h0[l], 4503599627370496.0)));  // exact small integer
-        }
-      }
-      if constexpr (NL == 3) {
-        if (swap) { const uint32_t t = u[0]; u[0] = u[2]; u[2] = t; }
-      }
-      Out o[NL];
-#pragma unroll
-      for (int l = 0; l < NL; ++l) {
-        if constexpr (AFFINE) {
-          float c[4], r[4];
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            c[k] = k < sig_n(SIG) ? acst[k][l] : 0.f;
-            r[k] = k < sig_n(SIG) ? arcp[k][l] : 0.f;
-          }
-          o[l] = Out(__float_as_uint(sig_apply<SIG>(float(u[l]), c, r)));  // Cast u8 -> f32, chain
-        } else {
-          o[l] = lut[l][u[l]];
-        }
-      }
-      const bool al = (w.flags & WF_LANE_ALIGNED) != 0;
-      if constexpr (SPLIT) {  // split_block, ops.cpp:402-424
-#pragma unroll
-        for (int l = 0; l < 3; ++l) {
-          uint8_t* p = reinterpret_cast<uint8_t*>(w.dst[l]) + uint64_t(y) * w.pitch[l] + uint64_t(x) * OB;
-          if constexpr (OLK == FK_F32) {
-            if (al) {
-              if (st) __stcs(reinterpret_cast<float*>(p), __uint_as_float(uint32_t(o[l])));
-              else *reinterpret_cast<uint32_t*>(p) = uint32_t(o[l]);
-              continue;
-            }
-          }
-          dev::store_lane<OLK, Out>(p, o[l], al);
-        }
-      } else {  // store_block, ops.cpp:396-400
-        uint8_t* p = reinterpret_cast<uint8_t*>(w.dst[0]) + uint64_t(y) * w.pitch[0] + uint64_t(x) * OB * NL;
-#pragma unroll
-        for (int l = 0; l < NL; ++l) dev::store_lane<OLK, Out>(p + l * OB, o[l], al);
-      }
+      column_tap<NL, OLK, SPLIT, SIG, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut, al);
     }
   }
 }
