@@ -97,7 +97,7 @@ __device__ __forceinline__ void row_taps(const uint8_t* row, const ColGeom& g, u
 // The chain after the u8 read, on the lanes of one output pixel.
 template <int NL, uint32_t OLK, uint32_t SIG, class Out>
 __device__ __forceinline__ void chain(uint32_t (&u)[3], bool swap, const float (&acst)[4][3], const float (&arcp)[4][3],
-                                      const Out (*lut)[256], Out (&o)[NL]) {
+                                      const Out* lut, Out (&o)[NL]) {
   if constexpr (NL == 3) {
     if (swap) { const uint32_t t = u[0]; u[0] = u[2]; u[2] = t; }
   }
@@ -112,7 +112,7 @@ __device__ __forceinline__ void chain(uint32_t (&u)[3], bool swap, const float (
       }
       o[l] = Out(__float_as_uint(sig_apply<SIG>(float(u[l]), c, r)));  // Cast u8 -> f32, chain
     } else {
-      o[l] = lut[l][u[l]];
+      o[l] = lut[l * 256 + u[l]];
     }
   }
 }
@@ -143,7 +143,7 @@ __device__ __forceinline__ void store_px(const DWrite& w, uint32_t x, uint32_t y
 template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool ALIGNED, class Out>
 __device__ __forceinline__ void column_bilinear(const DSample& s, const DWrite& w, const RowEnt* rows, uint32_t x,
                                                 uint32_t y0, uint32_t y1, bool swap, const float (&acst)[4][3],
-                                                const float (&arcp)[4][3], const Out (*lut)[256], bool al) {
+                                                const float (&arcp)[4][3], const Out* lut, bool al) {
   const XEnt xe = dev::x_entry(s, x, NL);
   const ColGeom g = col_geom(xe.o0, xe.o1);
   const uint8_t* base = reinterpret_cast<const uint8_t*>(s.src);
@@ -190,7 +190,7 @@ __device__ __forceinline__ void column_bilinear(const DSample& s, const DWrite& 
 template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, class Out>
 __device__ __forceinline__ void column_tap(const DSample& s, const DWrite& w, const RowEnt* rows, uint32_t x,
                                            uint32_t y0, uint32_t y1, bool swap, const float (&acst)[4][3],
-                                           const float (&arcp)[4][3], const Out (*lut)[256], bool al) {
+                                           const float (&arcp)[4][3], const Out* lut, bool al) {
   const uint32_t o0 = s.mode == RD_DIRECT ? (s.x0 + x) * NL : dev::x_entry(s, x, NL).o0;
   const uint8_t* base = reinterpret_cast<const uint8_t*>(s.src) + o0;
   for (uint32_t y = y0; y < y1; ++y) {
@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256) fk_resample_sep(const __grid_constant__ D
   constexpr bool AFFINE = SIG != kSigLut;
   using Out = typename std::conditional<OLK == FK_F64, uint64_t, uint32_t>::type;
   __shared__ RowEnt rows[kBandMax];
-  __shared__ Out lut[AFFINE ? 1 : NL][AFFINE ? 1 : 256];
+  __shared__ Out lut[AFFINE ? 1 : NL * 256];
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t y_begin = blockIdx.y * P.tiles_per_cta;  // tiles_per_cta = band rows for this kernel
   const uint32_t y_end = min(y_begin + P.tiles_per_cta, P.height);
@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(256) fk_resample_sep(const __grid_constant__ D
         dev::run_ops(P, s.post_off, s.post_len, z, v);
         dev::run_ops(P, P.op_base, P.n_ops, z, v);
 #pragma unroll
-        for (int l = 0; l < NL; ++l) lut[l][t] = Out(v[0][l]);
+        for (int l = 0; l < NL; ++l) lut[l * 256 + t] = Out(v[0][l]);
       }
     }
     __syncthreads();
