@@ -610,6 +610,16 @@ void fill_plan_io(DPlan& P, const DeviceProgram& dp, const Pipeline& p, const fk
 
 bool lut_allowed(const fk_exec_config* cfg) { return !(cfg && (cfg->flags & FK_EXEC_NO_LUT)); }
 
+// FK_PREFER_LUT=1 runs u8 AFFINE chains through the 256-entry table instead
+// (A/B profiling of LDS lookups vs in-register FP32 ops).
+bool lut_preferred() {
+  static const bool on = [] {
+    const char* e = std::getenv("FK_PREFER_LUT");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // FK_RESAMPLE_TILES=1 selects the earlier tile-per-thread resample kernel
 // (fk_resample.cu) instead of the column-streaming one, for A/B profiling.
 bool tile_resample() {
@@ -641,7 +651,7 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
   const bool generic_only = cfg && (cfg->flags & FK_EXEC_FORCE_GENERIC);
   // kernel selection: a registered compiled chain first, the interpreter otherwise
   const bool direct = dp.direct_ok && !generic_only;
-  const bool affine = !direct && dp.affine_ok && !generic_only;
+  const bool affine = !direct && dp.affine_ok && !generic_only && !lut_preferred();
   const bool compiled = affine || (!direct && dp.resample_ok && lut_allowed(cfg) && !generic_only);
   const int cls = generic_state_class(dp.fused_wide, dp.fused_lanes);
   DPlan P = base_plan(p.space.width, p.space.height, p.space.batch, dp.read_flat && dp.write_flat,
