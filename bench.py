@@ -130,14 +130,18 @@ def build(lib, workload: str, rank: int, crops: int, n_ops: int, world: int = 1,
     return wl.crops_224(lib, hi - lo, per_crop_norm=False, name="C5", first=lo)
 
 
+def workload_name(workload, crops, n_ops):
+    return {"c1": "configs[0] C1: 3840x2160 f32 -> mul,add,sub,div,cast -> u8 (vertical fusion)",
+            "c2": "configs[1] C2: cvGS 50 crops of 1920x1080 u8x3 -> bilinear 64x128 -> SwapRB -> f32 -> "
+                  "normalize -> split",
+            "c3": f"configs[2] C3: {n_ops} chained f32 ops on 4096x4096",
+            "c4": f"configs[3] C4: {crops} crops 224x224x3 per GPU, per-crop resize + per-crop normalize, split",
+            "c5": f"configs[4] C5: {crops} crops 224x224x3 per GPU, crop->bilinear resize->cast f32->normalize"
+                  "->split (cvGS chain at B200 scale)"}[workload]
+
+
 def describe(w, workload, crops, n_ops, world):
-    d = {"c1": "configs[0] C1: 3840x2160 f32 -> mul,add,sub,div,cast -> u8 (vertical fusion)",
-         "c2": "configs[1] C2: cvGS 50 crops of 1920x1080 u8x3 -> bilinear 64x128 -> SwapRB -> f32 -> "
-               "normalize -> split",
-         "c3": f"configs[2] C3: {n_ops} chained f32 ops on 4096x4096",
-         "c4": f"configs[3] C4: {crops} crops 224x224x3 per GPU, per-crop resize + per-crop normalize, split",
-         "c5": f"configs[4] C5: {crops} crops 224x224x3 per GPU, crop->bilinear resize->cast f32->normalize"
-               "->split (cvGS chain at B200 scale)"}[workload]
+    d = workload_name(workload, crops, n_ops)
     cfg = {"workload": d, "points_per_gpu": w.points, "alg_bytes_per_gpu": w.alg_bytes,
            "out_bytes_per_gpu": w.out_bytes, "in_bytes_per_gpu": w.in_bytes,
            "parallelism": f"batch-sharded x{world}, no collective" if world > 1 else "1 GPU",
@@ -211,7 +215,8 @@ def main():
         line = {"metric": METRIC, "value": cpu["value"], "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": mean * 1e3, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-                "config": {"workload": args.workload, "sample": cpu["sample"]},
+                "config": {"workload": workload_name(args.workload, args.crops, args.n_ops),
+                           "sample": cpu["sample"], "parallelism": "host cores (OpenMP), rank 0 only"},
                 "impl": "reference", "cpu_baseline": cpu,
                 "e2e": {"value": cpu["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
         print(json.dumps(line))
