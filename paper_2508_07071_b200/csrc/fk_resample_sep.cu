@@ -51,10 +51,12 @@ __device__ __forceinline__ ColGeom col_geom(uint32_t o0, uint32_t o1) {
   return ColGeom{o0 & ~3u, 8 * r, 8 * (r + (o1 - o0)), last >= 4 ? 1u : 0u, last >= 8 ? 1u : 0u};
 }
 
+// Load *p only if `need` (the value is unspecified otherwise; callers use only
+// bytes of words they need).
 __device__ __forceinline__ uint32_t ld_if(const uint32_t* p, uint32_t need) {
-  uint32_t v = 0;
+  uint32_t v;
   asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t@q ld.global.nc.u32 %0, [%1];\n\t}"
-               : "+r"(v) : "l"(p), "r"(need));
+               : "=r"(v) : "l"(p), "r"(need));
   return v;
 }
 
@@ -117,82 +119,129 @@ __device__ __forceinline__ void chain(uint32_t (&u)[3], bool swap, const float (
   }
 }
 
-template <int NL, uint32_t OLK, bool SPLIT, class Out>
-__device__ __forceinline__ void store_px(const DWrite& w, uint32_t x, uint32_t y, const Out (&o)[NL], bool al) {
-  constexpr int OB = OLK == FK_U8 ? 1 : (OLK == FK_F32 ? 4 : 8);
-  if constexpr (SPLIT) {  // split_block, ops.cpp:402-424
+// Destination cursor of one output column: the byte address of (x, y) in each
+// destination plane, advanced by the pitch per output row.
+template <int NL, uint32_t OLK, bool SPLIT>
+struct ColOut {
+  static constexpr int OB = OLK == FK_U8 ? 1 : (OLK == FK_F32 ? 4 : 8);
+  static constexpr int ND = SPLIT ? 3 : 1;
+  uint8_t* p[ND];
+  uint64_t pitch[ND];
+  __device__ __forceinline__ ColOut(const DWrite& w, uint32_t x, uint32_t y) {
 #pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      uint8_t* p = reinterpret_cast<uint8_t*>(w.dst[l]) + uint64_t(y) * w.pitch[l] + uint64_t(x) * OB;
-      if constexpr (OLK == FK_F32) {
-        if (al) {
-          __stcs(reinterpret_cast<float*>(p), __uint_as_float(uint32_t(o[l])));
-          continue;
-        }
-      }
-      dev::store_lane<OLK, Out>(p, o[l], al);
+    for (int d = 0; d < ND; ++d) {
+      pitch[d] = w.pitch[d];
+      p[d] = reinterpret_cast<uint8_t*>(w.dst[d]) + uint64_t(y) * w.pitch[d] + uint64_t(x) * OB * (SPLIT ? 1 : NL);
     }
-  } else {  // store_block, ops.cpp:396-400
-    uint8_t* p = reinterpret_cast<uint8_t*>(w.dst[0]) + uint64_t(y) * w.pitch[0] + uint64_t(x) * OB * NL;
-#pragma unroll
-    for (int l = 0; l < NL; ++l) dev::store_lane<OLK, Out>(p + l * OB, o[l], al);
   }
+  // split_block (ops.cpp:402-424) / store_block (:396-400) of one pixel, then next row
+  template <bool AL, class Out>
+  __device__ __forceinline__ void put(const Out (&o)[NL]) {
+    if constexpr (SPLIT) {
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        if constexpr (OLK == FK_F32 && AL) __stcs(reinterpret_cast<float*>(p[l]), __uint_as_float(uint32_t(o[l])));
+        else dev::store_lane<OLK, Out>(p[l], o[l], AL);
+        p[l] += pitch[l];
+      }
+    } else {
+#pragma unroll
+      for (int l = 0; l < NL; ++l) dev::store_lane<OLK, Out>(p[0] + l * OB, o[l], AL);
+      p[0] += pitch[0];
+    }
+  }
+};
+
+// V-lerp top + (bot - top) * fy per lane (ops.cpp:296), round_clamp_u8 (res is
+// in [0, 255]), the chain, the store.
+template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool AL, class Out>
+__device__ __forceinline__ void emit(const double (&top)[3], const double (&bot)[3], double fy, bool swap,
+                                     const float (&acst)[4][3], const float (&arcp)[4][3], const Out* lut,
+                                     ColOut<NL, OLK, SPLIT>& out) {
+  uint32_t u[3];
+#pragma unroll
+  for (int l = 0; l < NL; ++l) {
+    const double res = __dadd_rn(top[l], __dmul_rn(__dsub_rn(bot[l], top[l]), fy));
+    u[l] = uint32_t(__double2loint(__dadd_rn(res, 6755399441055744.0)));
+  }
+  Out o[NL];
+  chain<NL, OLK, SIG, Out>(u, swap, acst, arcp, lut, o);
+  out.template put<AL>(o);
 }
 
-// Walk output rows [y0, y1) of column x: bilinear, source rows 4-byte aligned or not.
-template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool ALIGNED, class Out>
+// Walk output rows [y0, y1) of column x (bilinear). hA / hB hold the H-lerps of
+// source rows rA / rB; in state 0 hA is the top row, in state 1 hB is. When the
+// next output row moves down by one source row (the common case for scales in
+// (0.5, 2)) the old bottom becomes the new top by flipping the state, and only
+// the new bottom row's H-lerp is computed — no register copies.
+template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool ALIGNED, bool AL, class Out>
 __device__ __forceinline__ void column_bilinear(const DSample& s, const DWrite& w, const RowEnt* rows, uint32_t x,
                                                 uint32_t y0, uint32_t y1, bool swap, const float (&acst)[4][3],
-                                                const float (&arcp)[4][3], const Out* lut, bool al) {
+                                                const float (&arcp)[4][3], const Out* lut) {
   const XEnt xe = dev::x_entry(s, x, NL);
   const ColGeom g = col_geom(xe.o0, xe.o1);
   const uint8_t* base = reinterpret_cast<const uint8_t*>(s.src);
-  uint32_t held0 = 0xffffffffu, held1 = 0xffffffffu;  // source rows whose H-lerps h0 / h1 hold
-  double h0[3] = {0, 0, 0}, h1[3] = {0, 0, 0};
+  ColOut<NL, OLK, SPLIT> out(w, x, y0);
+  auto load = [&](uint32_t row, double (&h)[3]) {
+    uint32_t a, b;
+    row_taps<NL, ALIGNED>(base + uint64_t(row) * s.pitch, g, xe.o0, xe.o1, a, b);
+    hlerp<NL>(a, b, xe.f, h);
+  };
+  uint32_t rA = 0xffffffffu, rB = 0xffffffffu;
+  double hA[3] = {0, 0, 0}, hB[3] = {0, 0, 0};
+  bool state1 = false;
   for (uint32_t y = y0; y < y1; ++y) {
     const RowEnt re = rows[y - y0];
-    // rows only move down: the new top row is the held top, the held bottom, or new
-    if (re.s0 != held0) {
-      if (re.s0 == held1) {
-#pragma unroll
-        for (int l = 0; l < 3; ++l) h0[l] = h1[l];
+    if (!state1) {  // top = A, bottom = B
+      if (re.s0 == rA && re.s1 == rB) {
+      } else if (re.s0 == rB && re.s1 != rB) {  // moved down one row: B becomes the top
+        load(re.s1, hA);
+        rA = re.s1;
+        state1 = true;
+        emit<NL, OLK, SPLIT, SIG, AL, Out>(hB, hA, re.f, swap, acst, arcp, lut, out);
+        continue;
       } else {
-        uint32_t a, b;
-        row_taps<NL, ALIGNED>(base + uint64_t(re.s0) * s.pitch, g, xe.o0, xe.o1, a, b);
-        hlerp<NL>(a, b, xe.f, h0);
-      }
-      held0 = re.s0;
-    }
-    if (re.s1 != held1) {
-      if (re.s1 == re.s0) {
+        if (re.s0 != rA) { load(re.s0, hA); rA = re.s0; }
+        if (re.s1 == re.s0) {
 #pragma unroll
-        for (int l = 0; l < 3; ++l) h1[l] = h0[l];
+          for (int l = 0; l < 3; ++l) hB[l] = hA[l];
+        } else if (re.s1 != rB) {
+          load(re.s1, hB);
+        }
+        rB = re.s1;
+      }
+      emit<NL, OLK, SPLIT, SIG, AL, Out>(hA, hB, re.f, swap, acst, arcp, lut, out);
+    } else {        // top = B, bottom = A
+      if (re.s0 == rB && re.s1 == rA) {
+      } else if (re.s0 == rA && re.s1 != rA) {  // moved down one row: A becomes the top
+        load(re.s1, hB);
+        rB = re.s1;
+        state1 = false;
+        emit<NL, OLK, SPLIT, SIG, AL, Out>(hA, hB, re.f, swap, acst, arcp, lut, out);
+        continue;
       } else {
-        uint32_t a, b;
-        row_taps<NL, ALIGNED>(base + uint64_t(re.s1) * s.pitch, g, xe.o0, xe.o1, a, b);
-        hlerp<NL>(a, b, xe.f, h1);
-      }
-      held1 = re.s1;
-    }
-    uint32_t u[3];
+        if (re.s0 != rB) { load(re.s0, hB); rB = re.s0; }
+        if (re.s1 == re.s0) {
 #pragma unroll
-    for (int l = 0; l < NL; ++l) {  // top + (bot - top) * fy, round_clamp_u8 (res in [0, 255])
-      const double res = __dadd_rn(h0[l], __dmul_rn(__dsub_rn(h1[l], h0[l]), re.f));
-      u[l] = uint32_t(__double2loint(__dadd_rn(res, 6755399441055744.0)));
+          for (int l = 0; l < 3; ++l) hA[l] = hB[l];
+        } else if (re.s1 != rA) {
+          load(re.s1, hA);
+        }
+        rA = re.s1;
+      }
+      emit<NL, OLK, SPLIT, SIG, AL, Out>(hB, hA, re.f, swap, acst, arcp, lut, out);
     }
-    Out o[NL];
-    chain<NL, OLK, SIG, Out>(u, swap, acst, arcp, lut, o);
-    store_px<NL, OLK, SPLIT, Out>(w, x, y, o, al);
   }
 }
 
 // Nearest / non-resizing planes: one tap per output pixel.
-template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, class Out>
+template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool AL, class Out>
 __device__ __forceinline__ void column_tap(const DSample& s, const DWrite& w, const RowEnt* rows, uint32_t x,
                                            uint32_t y0, uint32_t y1, bool swap, const float (&acst)[4][3],
-                                           const float (&arcp)[4][3], const Out* lut, bool al) {
+                                           const float (&arcp)[4][3], const Out* lut) {
   const uint32_t o0 = s.mode == RD_DIRECT ? (s.x0 + x) * NL : dev::x_entry(s, x, NL).o0;
   const uint8_t* base = reinterpret_cast<const uint8_t*>(s.src) + o0;
+  ColOut<NL, OLK, SPLIT> out(w, x, y0);
   for (uint32_t y = y0; y < y1; ++y) {
     const uint8_t* p = base + uint64_t(rows[y - y0].s0) * s.pitch;
     uint32_t u[3];
@@ -200,14 +249,14 @@ __device__ __forceinline__ void column_tap(const DSample& s, const DWrite& w, co
     for (int l = 0; l < NL; ++l) u[l] = __ldg(p + l);
     Out o[NL];
     chain<NL, OLK, SIG, Out>(u, swap, acst, arcp, lut, o);
-    store_px<NL, OLK, SPLIT, Out>(w, x, y, o, al);
+    out.template put<AL>(o);
   }
 }
 
 }  // namespace
 
 template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG>
-__global__ void __launch_bounds__(256) fk_resample_sep(const __grid_constant__ DPlan P) {
+__global__ void __launch_bounds__(256, 4) fk_resample_sep(const __grid_constant__ DPlan P) {
   constexpr bool AFFINE = SIG != kSigLut;
   using Out = typename std::conditional<OLK == FK_F64, uint64_t, uint32_t>::type;
   __shared__ RowEnt rows[kBandMax];
@@ -265,12 +314,16 @@ __global__ void __launch_bounds__(256) fk_resample_sep(const __grid_constant__ D
     const bool al = (w.flags & WF_LANE_ALIGNED) != 0;
     const bool aligned_rows = ((s.src | s.pitch) & 3) == 0;
     if (s.mode == RD_BILINEAR) {
-      if (aligned_rows)
-        column_bilinear<NL, OLK, SPLIT, SIG, true, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut, al);
+      if (aligned_rows && al)
+        column_bilinear<NL, OLK, SPLIT, SIG, true, true, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut);
+      else if (al)
+        column_bilinear<NL, OLK, SPLIT, SIG, false, true, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut);
       else
-        column_bilinear<NL, OLK, SPLIT, SIG, false, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut, al);
+        column_bilinear<NL, OLK, SPLIT, SIG, false, false, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut);
+    } else if (al) {
+      column_tap<NL, OLK, SPLIT, SIG, true, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut);
     } else {
-      column_tap<NL, OLK, SPLIT, SIG, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut, al);
+      column_tap<NL, OLK, SPLIT, SIG, false, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut);
     }
   }
 }
