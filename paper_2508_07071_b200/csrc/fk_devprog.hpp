@@ -100,6 +100,9 @@ struct DPlan {
   uint32_t def_kind;         // kind of the BatchRead default value
   uint32_t op_base;          // compute ops are table[op_base, op_base + n_ops); post ops at DSample::post_off
   uint64_t def[3];           // BatchRead default Element (ops.hpp:111), lane-encoded
+  float aff_c[4][3];         // AFFINE chain constants per op and lane when no op is per-plane
+  float aff_r[4][3];         // ... and their reciprocals RN(1 / c)
+  uint32_t aff_inline;       // 1: aff_c / aff_r hold the chain's constants
 };
 
 }  // namespace fk

@@ -169,6 +169,8 @@ struct DeviceProgram {
   int resample_lanes = 0;
   bool affine_ok = false;        // ... in AFFINE mode: cast u8->f32 then a registered f32 chain
   uint32_t aff_base = 0, aff_n = 0, aff_sig = 0;
+  bool aff_inline = false;       // no AFFINE op is per-plane: constants go in the kernel parameters
+  float aff_c[4][3] = {}, aff_r[4][3] = {};
   bool direct_ok = false;        // the compiled f32 element-wise kernel can run the fused pass
   bool direct_u8 = false;        // ... ending in Cast f32 -> u8
   uint32_t dir_base = 0, dir_sig = 0;
@@ -400,6 +402,8 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
     for (const DSample& s : dp->reads)
       ok = ok && !(s.flags & SF_DEFAULT) && (s.flags & SF_LUT_SRC) && lanes_of(s.kind) == nl;
     ok = ok && lanes_of(uint32_t(p.write.in_kind)) == nl;
+    for (const DWrite& w : writes)  // the column-streaming kernel keeps 32-bit destination pitches
+      for (uint64_t pitch : w.pitch) ok = ok && pitch < (1ull << 32);
     dp->resample_ok = ok;
     dp->resample_lanes = nl;
     // AFFINE mode: [SwapRB | Cast u8->f32]* (exactly one cast, folded or not), then
@@ -444,6 +448,17 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
       dp->aff_base = uint32_t(dp->table.size());
       dp->aff_n = uint32_t(arith.size());
       dp->table.insert(dp->table.end(), arith.begin(), arith.end());
+      dp->aff_inline = true;
+      for (size_t k = 0; k < arith.size(); ++k) {
+        dp->aff_inline = dp->aff_inline && !arith[k].per_z;
+        for (int l = 0; l < 3; ++l) {
+          const uint32_t bits = uint32_t(arith[k].c[arith[k].nl == 3 ? l : 0]);
+          float c;
+          std::memcpy(&c, &bits, 4);
+          dp->aff_c[k][l] = c;
+          dp->aff_r[k][l] = 1.0f / c;  // IEEE RN, as __frcp_rn
+        }
+      }
     }
   }
   // direct f32 kernel: f32 planes read as-is, f32 arith runs (any repeat), an
@@ -677,6 +692,11 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
     uint64_t band = work / (148ull * 12);
     band = std::max<uint64_t>(4, std::min<uint64_t>(resample_sep_band_max(), band));
     DPlan S = P;
+    if (affine && dp.aff_inline) {
+      S.aff_inline = 1;
+      std::memcpy(S.aff_c, dp.aff_c, sizeof S.aff_c);
+      std::memcpy(S.aff_r, dp.aff_r, sizeof S.aff_r);
+    }
     S.width = W;
     S.height = H;
     S.tiles_per_cta = uint32_t(band);
