@@ -172,18 +172,20 @@ __device__ __forceinline__ void emit(const double (&top)[3], const double (&bot)
 
 // One source row's two taps, split into issue (the loads) and use (the byte
 // extraction) so the next row's loads are in flight while this row is lerped.
+// `at` is the column's gather address in that row: the first tap word for
+// aligned rows, the row start otherwise.
 template <int NL, bool ALIGNED>
 struct RowFetch {
   uint32_t w[3];
   const uint8_t* row;
-  __device__ __forceinline__ void issue(const uint8_t* r, const ColGeom& g) {
+  __device__ __forceinline__ void issue(const uint8_t* at, const ColGeom& g) {
     if constexpr (NL == 3 && ALIGNED) {
-      const uint32_t* p = reinterpret_cast<const uint32_t*>(r + g.woff);
+      const uint32_t* p = reinterpret_cast<const uint32_t*>(at);
       w[0] = __ldg(p);
       w[1] = ld_if(p + 1, g.need1);
       w[2] = ld_if(p + 2, g.need2);
     } else {
-      row = r;
+      row = at;
     }
   }
   __device__ __forceinline__ void taps(const ColGeom& g, uint32_t o0, uint32_t o1, uint32_t& a, uint32_t& b) const {
@@ -196,30 +198,31 @@ struct RowFetch {
   }
 };
 
-// Source rows a band visits, in order, and the output rows each one completes:
-// output row k (source rows s0 <= s1) is emitted right after visiting s1, with
-// the previous visit being s0 (or s1 itself when s0 == s1, the clamped edge).
-struct Visit {
-  uint32_t row;    // source row (absolute)
-  uint32_t k_end;  // output rows [previous k_end, k_end) are emitted at this visit
+// The source rows a band visits, in order (byte offsets voff[]), and the output
+// rows each visit completes: output row k (source rows s0, s1) is emitted right
+// after the visits s0, s1 — the last two visits are always exactly (s0, s1),
+// so an edge row whose s0 == s1 (clamped) visits that row twice. Output rows
+// [vend[v - 1], vend[v]) are emitted at visit v. voff[nv] repeats voff[nv - 1]
+// (the walk prefetches one visit ahead).
+struct Visits {
+  uint64_t voff[2 * kBandMax + 1];
+  uint32_t vend[2 * kBandMax];
+  uint32_t n;
 };
 
-// Built by warp 0 for the band's n output rows. Source rows are clamped
-// floor(cy) / floor(cy) + 1 (y_entry), so s1 is s0 or s0 + 1 and both are
-// non-decreasing in k: the visits are the distinct rows of all {s0, s1} in
-// order, output row k (s0 != s1) finds s0 as the visit just before s1, and
-// output row k introduces at most the two new rows s0 (> s1 of row k - 1) and s1.
-__device__ __forceinline__ uint32_t build_visits_warp(const RowEnt* rows, uint32_t n, Visit* vis) {
+// Built by warp 0 for the band's n output rows. Output row k adds no visit when
+// (s0, s1) equals row k - 1's, one visit (s1) when its s0 is row k - 1's s1,
+// two (s0, s1) otherwise; a warp scan places them.
+__device__ __forceinline__ void build_visits_warp(const RowEnt* rows, uint32_t n, uint64_t pitch, Visits& V) {
   const uint32_t lane = threadIdx.x & 31u;
   uint32_t base = 0;
   for (uint32_t c = 0; c < n; c += 32) {
     const uint32_t k = c + lane;
     const bool in = k < n;
     const uint32_t s0 = in ? rows[k].s0 : 0, s1 = in ? rows[k].s1 : 0;
-    const uint32_t p1 = (in && k > 0) ? rows[k - 1].s1 : 0;
-    const bool new0 = in && (k == 0 || s0 > p1);
-    const bool new1 = in && s1 != s0 && (k == 0 || s1 > p1);
-    const uint32_t cnt = uint32_t(new0) + uint32_t(new1);
+    const bool first = k == 0;
+    const uint32_t p0 = (in && !first) ? rows[k - 1].s0 : 0, p1 = (in && !first) ? rows[k - 1].s1 : 0;
+    const uint32_t cnt = !in ? 0u : (!first && s0 == p0 && s1 == p1) ? 0u : (!first && s0 == p1) ? 1u : 2u;
     uint32_t incl = cnt;
 #pragma unroll
     for (uint32_t d = 1; d < 32; d <<= 1) {
@@ -227,15 +230,21 @@ __device__ __forceinline__ uint32_t build_visits_warp(const RowEnt* rows, uint32
       if (lane >= d) incl += t;
     }
     const uint32_t pos = base + incl - cnt;
-    if (new0) vis[pos] = Visit{s0, k};
-    if (new1) vis[pos + uint32_t(new0)] = Visit{s1, k};
+    if (cnt == 2) {
+      V.voff[pos] = uint64_t(s0) * pitch;
+      V.vend[pos] = k;
+    }
+    if (cnt != 0) V.voff[pos + cnt - 1] = uint64_t(s1) * pitch;
     __syncwarp();
-    // the last output row of each s1 closes that visit (the visit last created so far)
-    if (in && (k + 1 == n || rows[k + 1].s1 != s1)) vis[pos + cnt - 1].k_end = k + 1;
-    __syncwarp();
+    // the last output row attached to a visit closes it
+    if (in && (k + 1 == n || rows[k + 1].s0 != s0 || rows[k + 1].s1 != s1)) V.vend[pos + cnt - 1] = k + 1;
     base += __shfl_sync(0xffffffffu, incl, 31);
+    __syncwarp();
   }
-  return base;
+  if (lane == 0) {
+    V.voff[base] = V.voff[base - 1];
+    V.n = base;
+  }
 }
 
 // Walk the band's visits for column x (bilinear). Each visit H-lerps ONE source
@@ -244,29 +253,26 @@ __device__ __forceinline__ uint32_t build_visits_warp(const RowEnt* rows, uint32
 // by unrolling the walk by two, so no H-lerp is ever copied between registers.
 template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool ALIGNED, bool AL, class Out>
 __device__ __forceinline__ void column_bilinear(const DSample& s, const DWrite& w, const RowEnt* rows,
-                                                const Visit* vis, uint32_t nv, uint32_t x, uint32_t y0, bool swap,
+                                                const Visits& V, uint32_t x, uint32_t y0, bool swap,
                                                 const float (&acst)[4][3], const float (&arcp)[4][3],
                                                 const Out* lut) {
   const XEnt xe = dev::x_entry(s, x, NL);
   const ColGeom g = col_geom(xe.o0, xe.o1);
-  const uint8_t* base = reinterpret_cast<const uint8_t*>(s.src);
+  const uint8_t* col = reinterpret_cast<const uint8_t*>(s.src) + (NL == 3 && ALIGNED ? g.woff : 0u);
   ColOut<NL, OLK, SPLIT> out(w, x, y0);
   RowFetch<NL, ALIGNED> F;
-  F.issue(base + uint64_t(vis[0].row) * s.pitch, g);
+  F.issue(col + V.voff[0], g);
   double hA[3] = {0, 0, 0}, hB[3] = {0, 0, 0};
   uint32_t k = 0;
+  const uint32_t nv = V.n;
   // visit v: H-lerp its row into `cur`, prefetch visit v + 1, emit its outputs
   auto visit = [&](uint32_t v, double (&cur)[3], const double (&prev)[3]) {
     uint32_t a, b;
     F.taps(g, xe.o0, xe.o1, a, b);
-    const Visit e = vis[v];
-    F.issue(base + uint64_t(vis[v + 1 < nv ? v + 1 : v].row) * s.pitch, g);
+    F.issue(col + V.voff[v + 1], g);
     hlerp<NL>(a, b, xe.f, cur);
-    for (; k < e.k_end; ++k) {
-      const RowEnt re = rows[k];
-      if (re.s0 != re.s1) emit<NL, OLK, SPLIT, SIG, AL, Out>(prev, cur, re.f, swap, acst, arcp, lut, out);
-      else emit<NL, OLK, SPLIT, SIG, AL, Out>(cur, cur, re.f, swap, acst, arcp, lut, out);
-    }
+    for (const uint32_t e = V.vend[v]; k < e; ++k)
+      emit<NL, OLK, SPLIT, SIG, AL, Out>(prev, cur, rows[k].f, swap, acst, arcp, lut, out);
   };
   for (uint32_t v = 0; v < nv; v += 2) {
     visit(v, hA, hB);
@@ -310,8 +316,7 @@ __global__ void __launch_bounds__(256, 4) fk_resample_sep(const __grid_constant_
   constexpr bool AFFINE = SIG != kSigLut;
   using Out = typename std::conditional<OLK == FK_F64, uint64_t, uint32_t>::type;
   __shared__ RowEnt rows[kBandMax];
-  __shared__ Visit vis[2 * kBandMax];
-  __shared__ uint32_t n_vis;
+  __shared__ Visits vis;
   __shared__ Out lut[AFFINE ? 1 : NL * 256];
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t y_begin = blockIdx.y * P.tiles_per_cta;  // tiles_per_cta = band rows for this kernel
@@ -365,10 +370,7 @@ __global__ void __launch_bounds__(256, 4) fk_resample_sep(const __grid_constant_
     }
     __syncthreads();
     if (s.mode == RD_BILINEAR) {
-      if (threadIdx.x < 32) {
-        const uint32_t nv = build_visits_warp(rows, y_end - y_begin, vis);
-        if (threadIdx.x == 0) n_vis = nv;
-      }
+      if (threadIdx.x < 32) build_visits_warp(rows, y_end - y_begin, s.pitch, vis);
       __syncthreads();
     }
     if (!(w.flags & WF_ACTIVE) || x >= P.width) continue;  // BatchWrite z >= active_count / past the row
@@ -376,11 +378,11 @@ __global__ void __launch_bounds__(256, 4) fk_resample_sep(const __grid_constant_
     const bool aligned_rows = ((s.src | s.pitch) & 3) == 0;
     if (s.mode == RD_BILINEAR) {
       if (aligned_rows && al)
-        column_bilinear<NL, OLK, SPLIT, SIG, true, true, Out>(s, w, rows, vis, n_vis, x, y_begin, swap, acst, arcp, lut);
+        column_bilinear<NL, OLK, SPLIT, SIG, true, true, Out>(s, w, rows, vis, x, y_begin, swap, acst, arcp, lut);
       else if (al)
-        column_bilinear<NL, OLK, SPLIT, SIG, false, true, Out>(s, w, rows, vis, n_vis, x, y_begin, swap, acst, arcp, lut);
+        column_bilinear<NL, OLK, SPLIT, SIG, false, true, Out>(s, w, rows, vis, x, y_begin, swap, acst, arcp, lut);
       else
-        column_bilinear<NL, OLK, SPLIT, SIG, false, false, Out>(s, w, rows, vis, n_vis, x, y_begin, swap, acst, arcp, lut);
+        column_bilinear<NL, OLK, SPLIT, SIG, false, false, Out>(s, w, rows, vis, x, y_begin, swap, acst, arcp, lut);
     } else if (al) {
       column_tap<NL, OLK, SPLIT, SIG, true, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut);
     } else {
