@@ -28,9 +28,6 @@ cudaError_t launch_direct(uint32_t sig, bool to_u8, const DPlan& P, cudaStream_t
 uint32_t resample_sep_band_max();
 cudaError_t launch_resample_sep(int src_lanes, uint32_t out_lane_kind, bool split, uint32_t sig, const DPlan& P,
                                 uint32_t block, cudaStream_t st);
-// ... its AFFINE chains with per-plane constants (fk_resample_sep_pz.cu; P.aff_inline == 0)
-cudaError_t launch_resample_sep_pz(int src_lanes, bool split, uint32_t sig, const DPlan& P, dim3 grid,
-                                   uint32_t block, cudaStream_t st);
 
 bool resample_affine_registered(uint32_t sig);  // fk_sig.cuh FK_AFFINE_SIGS
 // sig == kSigLut: LUT mode; else the registered AFFINE chain signature

@@ -31,6 +31,9 @@ namespace fk {
 
 namespace {
 
+#ifndef FK_SEP_MINB
+#define FK_SEP_MINB 4  // resident CTAs per SM (64 registers per thread)
+#endif
 constexpr uint32_t kBandMax = 64;  // output rows per CTA (host picks <= this)
 
 struct RowEnt {                    // one output row: source rows (absolute) and fy
@@ -97,26 +100,17 @@ __device__ __forceinline__ void row_taps(const uint8_t* row, const ColGeom& g, u
   }
 }
 
-// The chain after the u8 read, on the lanes of one output pixel.
-template <int NL, uint32_t OLK, uint32_t SIG, class Out>
-__device__ __forceinline__ void chain(uint32_t (&u)[3], bool swap, const float (&acst)[4][3], const float (&arcp)[4][3],
-                                      const Out* lut, Out (&o)[NL]) {
-  if constexpr (NL == 3) {
-    if (swap) { const uint32_t t = u[0]; u[0] = u[2]; u[2] = t; }
-  }
+// The chain after the u8 read, on the lanes of one output pixel: one table
+// lookup per lane (the table holds the chain over all 256 byte values, slot m
+// = output lane sigma(m) from input lane m; see build_affine_table / the LUT
+// build in the kernel). Packed outputs put lane sigma(m) in place here; split
+// outputs swap their destination planes instead (ColOut).
+template <int NL, bool SPLIT, class Out>
+__device__ __forceinline__ void chain(const uint32_t (&u)[3], bool swap, const Out* lut, Out (&o)[NL]) {
 #pragma unroll
-  for (int l = 0; l < NL; ++l) {
-    if constexpr (SIG != kSigLut) {
-      float c[4], r[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        c[k] = k < sig_n(SIG) ? acst[k][l] : 0.f;
-        r[k] = k < sig_n(SIG) ? arcp[k][l] : 0.f;
-      }
-      o[l] = Out(__float_as_uint(sig_apply<SIG>(float(u[l]), c, r)));  // Cast u8 -> f32, chain
-    } else {
-      o[l] = lut[l * 256 + u[l]];
-    }
+  for (int l = 0; l < NL; ++l) o[l] = lut[l * 256 + u[l]];
+  if constexpr (NL == 3 && !SPLIT) {
+    if (swap) { const Out t = o[0]; o[0] = o[2]; o[2] = t; }
   }
 }
 
@@ -128,11 +122,13 @@ struct ColOut {
   static constexpr int ND = SPLIT ? 3 : 1;
   uint8_t* p[ND];
   uint32_t pitch[ND];  // < 2^32 (checked by the host)
-  __device__ __forceinline__ ColOut(const DWrite& w, uint32_t x, uint32_t y) {
+  __device__ __forceinline__ ColOut(const DWrite& w, uint32_t x, uint32_t y, bool swap) {
 #pragma unroll
     for (int d = 0; d < ND; ++d) {
-      pitch[d] = uint32_t(w.pitch[d]);
-      p[d] = reinterpret_cast<uint8_t*>(w.dst[d]) + uint64_t(y) * w.pitch[d] + uint64_t(x) * OB * (SPLIT ? 1 : NL);
+      const int e = (SPLIT && swap) ? 2 - d : d;  // split + lane swap: lane m goes to plane sigma(m)
+      pitch[d] = uint32_t(w.pitch[e]);
+      // one row above (x, y): put() advances first, then stores
+      p[d] = reinterpret_cast<uint8_t*>(w.dst[e]) + (uint64_t(y) - 1) * w.pitch[e] + uint64_t(x) * OB * (SPLIT ? 1 : NL);
     }
   }
   // split_block (ops.cpp:402-424) / store_block (:396-400) of one pixel, then next row
@@ -141,24 +137,23 @@ struct ColOut {
     if constexpr (SPLIT) {
 #pragma unroll
       for (int l = 0; l < 3; ++l) {
+        p[l] += pitch[l];
         if constexpr (OLK == FK_F32 && AL) __stcs(reinterpret_cast<float*>(p[l]), __uint_as_float(uint32_t(o[l])));
         else dev::store_lane<OLK, Out>(p[l], o[l], AL);
-        p[l] += pitch[l];
       }
     } else {
+      p[0] += pitch[0];
 #pragma unroll
       for (int l = 0; l < NL; ++l) dev::store_lane<OLK, Out>(p[0] + l * OB, o[l], AL);
-      p[0] += pitch[0];
     }
   }
 };
 
 // V-lerp top + (bot - top) * fy per lane (ops.cpp:296), round_clamp_u8 (res is
 // in [0, 255]), the chain, the store.
-template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool AL, class Out>
+template <int NL, uint32_t OLK, bool SPLIT, bool AL, class Out>
 __device__ __forceinline__ void emit(const double (&top)[3], const double (&bot)[3], double fy, bool swap,
-                                     const float (&acst)[4][3], const float (&arcp)[4][3], const Out* lut,
-                                     ColOut<NL, OLK, SPLIT>& out) {
+                                     const Out* lut, ColOut<NL, OLK, SPLIT>& out) {
   uint32_t u[3];
 #pragma unroll
   for (int l = 0; l < NL; ++l) {
@@ -166,7 +161,7 @@ __device__ __forceinline__ void emit(const double (&top)[3], const double (&bot)
     u[l] = uint32_t(__double2loint(__dadd_rn(res, 6755399441055744.0)));
   }
   Out o[NL];
-  chain<NL, OLK, SIG, Out>(u, swap, acst, arcp, lut, o);
+  chain<NL, SPLIT, Out>(u, swap, lut, o);
   out.template put<AL>(o);
 }
 
@@ -251,15 +246,14 @@ __device__ __forceinline__ void build_visits_warp(const RowEnt* rows, uint32_t n
 // row (a source row's H-lerp is computed once however many output rows use it)
 // and emits the output rows it completes. hA / hB alternate as the current row
 // by unrolling the walk by two, so no H-lerp is ever copied between registers.
-template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool ALIGNED, bool AL, class Out>
+template <int NL, uint32_t OLK, bool SPLIT, bool ALIGNED, bool AL, class Out>
 __device__ __forceinline__ void column_bilinear(const DSample& s, const DWrite& w, const RowEnt* rows,
                                                 const Visits& V, uint32_t x, uint32_t y0, bool swap,
-                                                const float (&acst)[4][3], const float (&arcp)[4][3],
                                                 const Out* lut) {
   const XEnt xe = dev::x_entry(s, x, NL);
   const ColGeom g = col_geom(xe.o0, xe.o1);
   const uint8_t* col = reinterpret_cast<const uint8_t*>(s.src) + (NL == 3 && ALIGNED ? g.woff : 0u);
-  ColOut<NL, OLK, SPLIT> out(w, x, y0);
+  ColOut<NL, OLK, SPLIT> out(w, x, y0, swap);
   RowFetch<NL, ALIGNED> F;
   F.issue(col + V.voff[0], g);
   double hA[3] = {0, 0, 0}, hB[3] = {0, 0, 0};
@@ -271,8 +265,9 @@ __device__ __forceinline__ void column_bilinear(const DSample& s, const DWrite& 
     F.taps(g, xe.o0, xe.o1, a, b);
     F.issue(col + V.voff[v + 1], g);
     hlerp<NL>(a, b, xe.f, cur);
+#pragma unroll 1
     for (const uint32_t e = V.vend[v]; k < e; ++k)
-      emit<NL, OLK, SPLIT, SIG, AL, Out>(prev, cur, rows[k].f, swap, acst, arcp, lut, out);
+      emit<NL, OLK, SPLIT, AL, Out>(prev, cur, rows[k].f, swap, lut, out);
   };
   for (uint32_t v = 0; v < nv; v += 2) {
     visit(v, hA, hB);
@@ -281,70 +276,87 @@ __device__ __forceinline__ void column_bilinear(const DSample& s, const DWrite& 
 }
 
 // Nearest / non-resizing planes: one tap per output pixel.
-template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool AL, class Out>
+template <int NL, uint32_t OLK, bool SPLIT, bool AL, class Out>
 __device__ __forceinline__ void column_tap(const DSample& s, const DWrite& w, const RowEnt* rows, uint32_t x,
-                                           uint32_t y0, uint32_t y1, bool swap, const float (&acst)[4][3],
-                                           const float (&arcp)[4][3], const Out* lut) {
+                                           uint32_t y0, uint32_t y1, bool swap, const Out* lut) {
   const uint32_t o0 = s.mode == RD_DIRECT ? (s.x0 + x) * NL : dev::x_entry(s, x, NL).o0;
   const uint8_t* base = reinterpret_cast<const uint8_t*>(s.src) + o0;
-  ColOut<NL, OLK, SPLIT> out(w, x, y0);
+  ColOut<NL, OLK, SPLIT> out(w, x, y0, swap);
   for (uint32_t y = y0; y < y1; ++y) {
     const uint8_t* p = base + uint64_t(rows[y - y0].s0) * s.pitch;
     uint32_t u[3];
 #pragma unroll
     for (int l = 0; l < NL; ++l) u[l] = __ldg(p + l);
     Out o[NL];
-    chain<NL, OLK, SIG, Out>(u, swap, acst, arcp, lut, o);
+    chain<NL, SPLIT, Out>(u, swap, lut, o);
     out.template put<AL>(o);
   }
 }
 
-using Cst = float[4][3];
-template <bool PZ>
-__device__ __forceinline__ const Cst& pick(const Cst& per_plane, const Cst& params) {
-  if constexpr (PZ) return per_plane;
-  else return params;
+// AFFINE table: slot m, entry t = the registered f32 chain (constants of output
+// lane sigma(m)) applied to float(t) — Cast u8 -> f32 then the chain, exactly
+// the per-pixel arithmetic, tabulated. Constants from the kernel parameters, or
+// the plane's BatchArith rows.
+template <int NL, uint32_t SIG, class Out>
+__device__ __forceinline__ void build_affine_table(const DPlan& P, uint32_t z, bool swap, Out* lut) {
+  float c[4][3], r[4][3];
+#pragma unroll
+  for (int k = 0; k < sig_n(SIG); ++k) {
+    if (P.aff_inline) {
+#pragma unroll
+      for (int l = 0; l < 3; ++l) { c[k][l] = P.aff_c[k][l]; r[k][l] = P.aff_r[k][l]; }
+    } else {
+      const DOp op = dev::prog_op(P, P.op_base + k);
+      uint64_t v[3] = {op.c[0], op.c[1], op.c[2]};
+      if (op.per_z) {
+        const uint64_t* row = reinterpret_cast<const uint64_t*>(op.per_z) + 3ull * (z < op.per_z_n ? z : op.per_z_n - 1);
+        v[0] = __ldg(row); v[1] = __ldg(row + 1); v[2] = __ldg(row + 2);
+      }
+#pragma unroll
+      for (int l = 0; l < 3; ++l) {
+        c[k][l] = __uint_as_float(uint32_t(v[op.nl == 3 ? l : 0]));
+        r[k][l] = __frcp_rn(c[k][l]);
+      }
+    }
+  }
+  for (uint32_t t = threadIdx.x; t < 256; t += blockDim.x) {
+#pragma unroll
+    for (int m = 0; m < NL; ++m) {
+      const int l = (NL == 3 && swap) ? 2 - m : m;
+      float cl[4], rl[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        cl[k] = k < sig_n(SIG) ? c[k][l] : 0.f;
+        rl[k] = k < sig_n(SIG) ? r[k][l] : 0.f;
+      }
+      lut[m * 256 + t] = Out(__float_as_uint(sig_apply<SIG>(float(t), cl, rl)));
+    }
+  }
 }
 
 }  // namespace
 
-// PZ: the AFFINE constants vary per plane (BatchArith), loaded per plane into
-// registers; otherwise they are read straight from the kernel parameters
-// (P.aff_c / P.aff_r: constant-bank operands, no registers held).
-template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool PZ>
-__global__ void __launch_bounds__(256, 4) fk_resample_sep(const __grid_constant__ DPlan P) {
+// One CTA = a strip of output columns x a band of rows, for the planes
+// blockIdx.z, blockIdx.z + gridDim.z, ... (horizontal fusion). SIG = a
+// registered AFFINE chain (table built from the compiled chain: once per CTA
+// when its constants are plane-independent), or kSigLut (table built per plane
+// by interpreting the plane's folded unaries + the compute program).
+template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG>
+__global__ void __launch_bounds__(256, FK_SEP_MINB) fk_resample_sep(const __grid_constant__ DPlan P) {
   constexpr bool AFFINE = SIG != kSigLut;
   using Out = typename std::conditional<OLK == FK_F64, uint64_t, uint32_t>::type;
   __shared__ RowEnt rows[kBandMax];
   __shared__ Visits vis;
-  __shared__ Out lut[AFFINE ? 1 : NL * 256];
+  __shared__ Out lut[NL * 256];
   const uint32_t x = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t y_begin = blockIdx.y * P.tiles_per_cta;  // tiles_per_cta = band rows for this kernel
   const uint32_t y_end = min(y_begin + P.tiles_per_cta, P.height);
+  int table_swap = -1;  // AFFINE with plane-independent constants: the swap the table was built for
   for (uint32_t zi = blockIdx.z; zi < P.batch; zi += gridDim.z) {
     const uint32_t z = P.order ? __ldg(P.order + zi) : zi;
     const DSample s = P.reads[z];
     const DWrite w = P.writes[z];
     const bool swap = ((s.flags & SF_POST_SWAP) != 0) != (P.prog_swap != 0);
-    float pz_c[4][3], pz_r[4][3];
-    if constexpr (AFFINE && PZ) {
-#pragma unroll
-      for (int k = 0; k < sig_n(SIG); ++k) {
-        const DOp op = dev::prog_op(P, P.op_base + k);
-        uint64_t c[3] = {op.c[0], op.c[1], op.c[2]};
-        if (op.per_z) {
-          const uint64_t* row = reinterpret_cast<const uint64_t*>(op.per_z) + 3ull * (z < op.per_z_n ? z : op.per_z_n - 1);
-          c[0] = __ldg(row); c[1] = __ldg(row + 1); c[2] = __ldg(row + 2);
-        }
-#pragma unroll
-        for (int l = 0; l < 3; ++l) {
-          pz_c[k][l] = __uint_as_float(uint32_t(c[op.nl == 3 ? l : 0]));
-          pz_r[k][l] = __frcp_rn(pz_c[k][l]);
-        }
-      }
-    }
-    const Cst& acst = pick<PZ>(pz_c, P.aff_c);
-    const Cst& arcp = pick<PZ>(pz_r, P.aff_r);
     __syncthreads();
     for (uint32_t j = threadIdx.x; j < y_end - y_begin; j += blockDim.x) {
       RowEnt e;
@@ -359,13 +371,18 @@ __global__ void __launch_bounds__(256, 4) fk_resample_sep(const __grid_constant_
       }
       rows[j] = e;
     }
-    if constexpr (!AFFINE) {
+    if constexpr (AFFINE) {
+      if (!P.aff_inline || table_swap != int(swap)) {
+        build_affine_table<NL, SIG, Out>(P, z, swap, lut);
+        table_swap = P.aff_inline ? int(swap) : -1;
+      }
+    } else {
       for (uint32_t t = threadIdx.x; t < 256; t += blockDim.x) {  // the chain over every byte value
         uint64_t v[1][3] = {{t, t, t}};
         dev::run_ops(P, s.post_off, s.post_len, z, v);
         dev::run_ops(P, P.op_base, P.n_ops, z, v);
 #pragma unroll
-        for (int l = 0; l < NL; ++l) lut[l * 256 + t] = Out(v[0][l]);
+        for (int m = 0; m < NL; ++m) lut[m * 256 + t] = Out(v[0][(NL == 3 && swap) ? 2 - m : m]);
       }
     }
     __syncthreads();
@@ -378,31 +395,17 @@ __global__ void __launch_bounds__(256, 4) fk_resample_sep(const __grid_constant_
     const bool aligned_rows = ((s.src | s.pitch) & 3) == 0;
     if (s.mode == RD_BILINEAR) {
       if (aligned_rows && al)
-        column_bilinear<NL, OLK, SPLIT, SIG, true, true, Out>(s, w, rows, vis, x, y_begin, swap, acst, arcp, lut);
+        column_bilinear<NL, OLK, SPLIT, true, true, Out>(s, w, rows, vis, x, y_begin, swap, lut);
       else if (al)
-        column_bilinear<NL, OLK, SPLIT, SIG, false, true, Out>(s, w, rows, vis, x, y_begin, swap, acst, arcp, lut);
+        column_bilinear<NL, OLK, SPLIT, false, true, Out>(s, w, rows, vis, x, y_begin, swap, lut);
       else
-        column_bilinear<NL, OLK, SPLIT, SIG, false, false, Out>(s, w, rows, vis, x, y_begin, swap, acst, arcp, lut);
+        column_bilinear<NL, OLK, SPLIT, false, false, Out>(s, w, rows, vis, x, y_begin, swap, lut);
     } else if (al) {
-      column_tap<NL, OLK, SPLIT, SIG, true, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut);
+      column_tap<NL, OLK, SPLIT, true, Out>(s, w, rows, x, y_begin, y_end, swap, lut);
     } else {
-      column_tap<NL, OLK, SPLIT, SIG, false, Out>(s, w, rows, x, y_begin, y_end, swap, acst, arcp, lut);
+      column_tap<NL, OLK, SPLIT, false, Out>(s, w, rows, x, y_begin, y_end, swap, lut);
     }
   }
-}
-
-// Launch one instantiation (the .cu files choose which ones exist).
-template <uint32_t SIG, bool PZ>
-cudaError_t launch_sep_affine(int src_lanes, bool split, const DPlan& P, dim3 grid, uint32_t block, cudaStream_t st) {
-  if (src_lanes == 3 && split) fk_resample_sep<3, FK_F32, true, SIG, PZ><<<grid, block, 0, st>>>(P);
-  else if (src_lanes == 3) fk_resample_sep<3, FK_F32, false, SIG, PZ><<<grid, block, 0, st>>>(P);
-  else fk_resample_sep<1, FK_F32, false, SIG, PZ><<<grid, block, 0, st>>>(P);
-  return cudaGetLastError();
-}
-
-inline dim3 sep_grid(const DPlan& P, uint32_t block) {
-  return dim3((P.width + block - 1) / block, (P.height + P.tiles_per_cta - 1) / P.tiles_per_cta,
-              P.batch < 65535u ? P.batch : 65535u);
 }
 
 }  // namespace fk
