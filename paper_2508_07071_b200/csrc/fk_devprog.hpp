@@ -103,6 +103,16 @@ struct DPlan {
   float aff_c[4][3];         // AFFINE chain constants per op and lane when no op is per-plane
   float aff_r[4][3];         // ... and their reciprocals RN(1 / c)
   uint32_t aff_inline;       // 1: aff_c / aff_r hold the chain's constants
+  // column-streaming kernel (fk_resample_sep): CTA slice blockIdx.z runs planes
+  // slots[blockIdx.z * slots_per_cta + h] (h < slots_per_cta, kNoPlane = none) with
+  // threads [h * slot_threads, (h + 1) * slot_threads); slots == nullptr: plane
+  // order[blockIdx.z], one per CTA
+  const uint32_t* slots;
+  uint32_t slots_per_cta;    // 1, or 2 planes sharing one row/visit table (equal rect_h, mode, swap)
+  uint32_t slot_threads;     // threads per plane slot
+  uint32_t slices;           // CTA slices along z (slots != nullptr)
+  uint32_t no_stage;         // 1: column-streaming kernel uses direct tap loads (A/B; FK_SEP_NOSTAGE=1)
 };
+constexpr uint32_t kNoPlane = 0xffffffffu;
 
 }  // namespace fk

@@ -15,6 +15,7 @@
 #include <map>
 #include <mutex>
 #include <string>
+#include <tuple>
 
 #include "fk_core.hpp"
 #include "fk_exec.hpp"
@@ -166,6 +167,7 @@ struct DeviceProgram {
   bool fused_lut_ok = true;      // every fused op is lane-wise
   bool fused_swap = false;       // odd number of lane swaps in the fused program
   bool resample_ok = false;      // the compiled u8 resample/LUT kernel can run the fused pass
+  bool sep_ok = false;           // ... and the column-streaming variant (32-bit source pitches)
   int resample_lanes = 0;
   bool affine_ok = false;        // ... in AFFINE mode: cast u8->f32 then a registered f32 chain
   uint32_t aff_base = 0, aff_n = 0, aff_sig = 0;
@@ -178,6 +180,9 @@ struct DeviceProgram {
   DSample* d_reads = nullptr;
   DWrite* d_writes = nullptr;
   uint32_t* d_order = nullptr;   // plane visiting order (grouped by source), or null
+  uint32_t* d_slots2 = nullptr;  // column-streaming kernel: planes paired by (mode, rect_h, swap), kNoPlane = none
+  uint32_t n_slices2 = 0;        // ... number of pairs
+  int stage_ok[2] = {-1, -1};    // staged column walk valid for [single, dual] slices (-1: not yet computed)
   std::vector<void*> extra;      // BatchArith constant tables
   std::vector<DSample> reads;    // host copies
   bool read_flat = false, write_flat = false;
@@ -191,7 +196,7 @@ struct DeviceProgram {
 
   ~DeviceProgram() {
     for (void* p : {static_cast<void*>(d_table), static_cast<void*>(d_reads), static_cast<void*>(d_writes),
-                    static_cast<void*>(d_order)})
+                    static_cast<void*>(d_order), static_cast<void*>(d_slots2)})
       if (p) cudaFree(p);
     for (void* p : extra) cudaFree(p);
   }
@@ -406,6 +411,11 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
       for (uint64_t pitch : w.pitch) ok = ok && pitch < (1ull << 32);
     dp->resample_ok = ok;
     dp->resample_lanes = nl;
+    // the column-streaming kernel keeps 32-bit source pitches (row addresses are IMAD.WIDE)
+    bool sep = true;
+    for (const DSample& s : dp->reads)  // ... and 16-bit band-relative source rows
+      sep = sep && s.pitch < (1ull << 32) && s.rect_h < 65536 && s.out_h < 65536;
+    dp->sep_ok = sep;
     // AFFINE mode: [SwapRB | Cast u8->f32]* (exactly one cast, folded or not), then
     // only f32 Mul/Add/Sub/Div (no swap after the first one), at most 4 of them.
     bool aff = ok && lane_kind(uint32_t(p.write.in_kind)) == FK_F32;
@@ -513,6 +523,28 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
     bool identity = true;
     for (uint32_t z = 0; z < B; ++z) identity = identity && order[z] == z;
     if (!identity) dp->d_order = upload(order);
+    // Two-plane slots for the column-streaming kernel: planes whose row walk is
+    // identical (same read mode, rect_h and lane swap; out_h is uniform over the
+    // batch) share one CTA, in the source-grouped order above.
+    if (dp->resample_ok && dp->sep_ok) {
+      std::map<std::tuple<uint32_t, uint32_t, uint32_t>, uint32_t> open;  // key -> plane waiting for a partner
+      std::vector<uint32_t> slots;
+      for (uint32_t z : order) {
+        const DSample& r = dp->reads[z];
+        const auto key = std::make_tuple(r.mode, r.mode == RD_DIRECT ? 0u : r.rect_h, r.flags & SF_POST_SWAP);
+        auto it = open.find(key);
+        if (it == open.end()) {
+          open.emplace(key, uint32_t(slots.size()));
+          slots.push_back(z);
+          slots.push_back(kNoPlane);
+        } else {
+          slots[it->second + 1] = z;
+          open.erase(it);
+        }
+      }
+      dp->n_slices2 = uint32_t(slots.size() / 2);
+      dp->d_slots2 = upload(slots);
+    }
   }
   dp->traffic = analytic_traffic(p);
   dp->d_table = upload(dp->table);
@@ -647,6 +679,47 @@ bool tile_resample() {
 
 }  // namespace
 
+namespace {
+
+// Host mirror of x_entry (fk_stages.cuh): tap byte offsets of output column i.
+void host_taps(const DSample& s, uint32_t i, uint32_t bpe, uint32_t& o0, uint32_t& o1) {
+  const double cx = (double(i) + 0.5) * double(s.rect_w) / double(s.out_w) - 0.5;
+  const long long ix = (long long)std::floor(cx), maxx = (long long)s.rect_w - 1;
+  o0 = uint32_t((s.x0 + std::min(std::max(ix, 0ll), maxx)) * bpe);
+  o1 = uint32_t((s.x0 + std::min(std::max(ix + 1, 0ll), maxx)) * bpe);
+}
+
+// Can every warp of the column-streaming kernel use the staged (cp.async ring)
+// walk? Source rows 16-byte aligned, and each warp's span of source bytes per
+// plane slot fits its ring region (the whole row, or half when the warp holds
+// two slots) — the same arithmetic as stage_plan in fk_resample_sep.cuh.
+bool sep_stage_ok(const DeviceProgram& dp, uint32_t W, uint32_t T, uint32_t spc) {
+  const uint32_t row = resample_sep_ring_row();
+  const uint32_t warps = (spc * T + 31) / 32;
+  for (const DSample& s : dp.reads) {
+    if (s.mode != RD_BILINEAR) continue;
+    if (((s.src + uint64_t(s.y0) * s.pitch) | s.pitch) & 15) return false;
+    const uint32_t bpe = uint32_t(lanes_of(s.kind));
+    for (uint32_t wi = 0; wi < warps; ++wi) {
+      const uint32_t t0 = wi * 32, t1 = std::min(t0 + 32, spc * T);
+      const bool two = t0 / T != (t1 - 1) / T;
+      for (uint32_t h = t0 / T; h <= (t1 - 1) / T; ++h) {
+        const uint32_t p0 = std::max(t0, h * T) - h * T, p1 = std::min(t1, (h + 1) * T) - h * T;
+        const uint32_t c0 = 2 * p0, c1 = std::min(2 * p1, W);
+        if (c0 >= c1) continue;
+        uint32_t lo, x1, x2, hi;
+        host_taps(s, c0, bpe, lo, x1);
+        host_taps(s, c1 - 1, bpe, x2, hi);
+        hi += bpe;
+        if ((hi - (lo & ~15u) + 15) / 16 * 16 > (two ? row / 2 : row)) return false;
+      }
+    }
+  }
+  return true;
+}
+
+}  // namespace
+
 void check_config(const fk_exec_config* c) {  // executor.cpp:20-25
   if (!c) return;
   if (c->chunk_rows < 1) fail(FK_E_INVALID_CONFIG, "chunk_rows must be >= 1");
@@ -683,15 +756,36 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     r.path = FK_PATH_COMPILED;
-  } else if (compiled && !tile_resample()) {
-    // column-streaming kernel: 2D grid (column strips x row bands x planes)
+  } else if (compiled && dp.sep_ok && !tile_resample()) {
+    // column-streaming kernel: one warp per CTA, 32 column pairs x a band of rows
+    // of one z slice (one plane, or two planes of equal row structure side by side)
     const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
-    const uint32_t block = std::min<uint32_t>(256, (W + 31) / 32 * 32);
-    const uint64_t strips = (W + block - 1) / block;
-    const uint64_t work = uint64_t(H) * strips * B;
-    uint64_t band = work / (148ull * 12);
-    band = std::max<uint64_t>(4, std::min<uint64_t>(resample_sep_band_max(), band));
+    const uint32_t pairs = (W + 1) / 2;  // one lane per output column pair
+    const uint32_t w1 = (pairs + 31) / 32, w2 = (2 * pairs + 31) / 32;  // warps per slice
+    // two planes per slice when that fills the warps better (224 columns: 112
+    // pairs -> 7 full warps per two planes instead of 4 warps per plane)
+    const bool dual = dp.d_slots2 && double(2 * pairs) / (32.0 * w2) > double(pairs) / (32.0 * w1);
     DPlan S = P;
+    S.slots = dual ? dp.d_slots2 : nullptr;
+    S.slots_per_cta = dual ? 2u : 1u;
+    S.slot_threads = pairs;
+    S.slices = dual ? dp.n_slices2 : B;
+    int& stage_ok = dp.stage_ok[dual ? 1 : 0];
+    if (stage_ok < 0) stage_ok = sep_stage_ok(dp, W, pairs, dual ? 2u : 1u) ? 1 : 0;
+    static const bool no_stage = [] {
+      const char* e = std::getenv("FK_SEP_NOSTAGE");
+      return e && e[0] == '1';
+    }();
+    S.no_stage = no_stage ? 1u : 0u;
+    // band: whole planes (up to the table size) unless the batch is too small to
+    // give ~2 waves of 16 warps per SM
+    const uint64_t units = uint64_t(dual ? w2 : w1) * S.slices;
+    const uint64_t target = 148ull * 16 * 2;
+    uint64_t band = std::min<uint64_t>(H, resample_sep_band_max());
+    if (units < target) {
+      const uint64_t nb = (target + units - 1) / units;
+      band = std::max<uint64_t>(4, std::min<uint64_t>(band, (H + nb - 1) / nb));
+    }
     if (affine && dp.aff_inline) {
       S.aff_inline = 1;
       std::memcpy(S.aff_c, dp.aff_c, sizeof S.aff_c);
@@ -701,7 +795,7 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
     S.height = H;
     S.tiles_per_cta = uint32_t(band);
     cuda_check(launch_resample_sep(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)), P.write_mode == WR_SPLIT,
-                                   affine ? dp.aff_sig : kSigLut, S, block, st),
+                                   affine ? dp.aff_sig : kSigLut, S, stage_ok == 1 && !S.no_stage, st),
                "fk_resample_sep launch");
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);

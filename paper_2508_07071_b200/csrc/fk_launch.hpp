@@ -26,8 +26,12 @@ cudaError_t launch_direct(uint32_t sig, bool to_u8, const DPlan& P, cudaStream_t
 
 // compiled column-streaming u8 resample kernel (fk_resample_sep.cu); P.tiles_per_cta = band rows
 uint32_t resample_sep_band_max();
+// staged: every warp's source span fits the cp.async ring and source rows are
+// 16-byte aligned (the host checks, sep_stage_ok), so the kernel is built without
+// the direct-load walk
 cudaError_t launch_resample_sep(int src_lanes, uint32_t out_lane_kind, bool split, uint32_t sig, const DPlan& P,
-                                uint32_t block, cudaStream_t st);
+                                bool staged, cudaStream_t st);
+uint32_t resample_sep_ring_row();
 
 bool resample_affine_registered(uint32_t sig);  // fk_sig.cuh FK_AFFINE_SIGS
 // sig == kSigLut: LUT mode; else the registered AFFINE chain signature

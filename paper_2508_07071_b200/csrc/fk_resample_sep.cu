@@ -5,13 +5,22 @@
 namespace fk {
 
 uint32_t resample_sep_band_max() { return kBandMax; }
+uint32_t resample_sep_ring_row() { return kRingRow; }
 
 cudaError_t launch_resample_sep(int src_lanes, uint32_t out_lane_kind, bool split, uint32_t sig, const DPlan& P,
-                                uint32_t block, cudaStream_t st) {
+                                bool staged, cudaStream_t st) {
   if (P.width == 0 || P.height == 0 || P.batch == 0) return cudaSuccess;
-  const dim3 grid((P.width + block - 1) / block, (P.height + P.tiles_per_cta - 1) / P.tiles_per_cta,
-                  P.batch < 65535u ? P.batch : 65535u);
-#define FK_RS(NL, OLK, SP, S) fk_resample_sep<NL, OLK, SP, S><<<grid, block, 0, st>>>(P)
+  // one warp per CTA: 32 pair slots of a slice (P.slot_threads pairs per plane slot)
+  const uint32_t spc = P.slots ? P.slots_per_cta : 1u;
+  const uint32_t slices = P.slots ? P.slices : P.batch;
+  const dim3 grid((spc * P.slot_threads + 31) / 32, (P.height + P.tiles_per_cta - 1) / P.tiles_per_cta,
+                  slices < 65535u ? slices : 65535u);
+  const uint32_t block = 32;
+#define FK_RS(NL, OLK, SP, S)                                                     \
+  do {                                                                            \
+    if (staged) fk_resample_sep<NL, OLK, SP, S, true><<<grid, block, 0, st>>>(P); \
+    else fk_resample_sep<NL, OLK, SP, S, false><<<grid, block, 0, st>>>(P);       \
+  } while (0)
   if (sig != kSigLut) {
 #define FK_CASE(S)                                          \
   if (sig == (S)) {                                         \
