@@ -251,6 +251,29 @@ struct KPar {
   __device__ __forceinline__ float c(int l, int k) const { return P.aff_c[k][NL == 3 && SW ? 2 - l : l]; }
   __device__ __forceinline__ float r(int l, int k) const { return P.aff_r[k][NL == 3 && SW ? 2 - l : l]; }
 };
+// The same constants loaded once into registers the compiler must keep (it
+// otherwise reloads them from the constant bank on every output row).
+__device__ __forceinline__ float pinf(float v) {
+  asm volatile("" : "+f"(v));
+  return v;
+}
+template <int NL, uint32_t SIG, bool SW>
+struct KPin {
+  float cc[3][4], rr[3][4];
+  __device__ __forceinline__ explicit KPin(const DPlan& P) {
+#pragma unroll
+    for (int l = 0; l < 3; ++l)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int m = NL == 3 && SW ? 2 - l : l;
+        const bool used = l < NL && k < sig_n(SIG);
+        cc[l][k] = used ? pinf(P.aff_c[k][m]) : 0.f;
+        rr[l][k] = used && sig_fn(SIG, k) == AF_DIV ? pinf(P.aff_r[k][m]) : 0.f;
+      }
+  }
+  __device__ __forceinline__ float c(int l, int k) const { return cc[l][k]; }
+  __device__ __forceinline__ float r(int l, int k) const { return rr[l][k]; }
+};
 
 template <int NL, uint32_t SIG>
 __device__ __forceinline__ void load_affine(const DPlan& P, uint32_t z, bool swap, AffConsts& K) {
@@ -293,7 +316,7 @@ __device__ __forceinline__ void load_affine(const DPlan& P, uint32_t z, bool swa
 // exact rational ties common (up to ~1700 pairs, ~500 per warp). A lane whose
 // push finds the list full marks itself and recomputes its whole column pair
 // afterwards.
-constexpr uint32_t kFixCap = 1024;
+constexpr uint32_t kFixCap = 512;
 struct FixShared {
   uint32_t n;
   uint16_t e[kFixCap];
@@ -572,7 +595,10 @@ __device__ __forceinline__ void pair_bilinear(const DSample& s, const DWrite& w,
 // touch into a shared-memory ring kRing - 1 visits ahead with cp.async (16-byte
 // chunks, zero-filled past the crop's last byte so nothing beyond the plane is
 // read; no registers hold data in flight), and gathers taps from shared memory.
-constexpr uint32_t kRing = 8;       // staged source rows per warp
+#ifndef FK_RING
+#define FK_RING 4
+#endif
+constexpr uint32_t kRing = FK_RING;  // staged source rows per warp (kRing - 1 visits in flight)
 constexpr uint32_t kRingRow = 512;  // bytes per staged row: one slot's span, or two 256-byte halves
 
 __device__ __forceinline__ void cp_async16(uint32_t dst, uint64_t src, uint32_t n) {
@@ -653,47 +679,70 @@ __device__ __forceinline__ void pair_bilinear_staged(const DWrite& w, const Band
                                                      FixList& fix) {
   const uint64_t fx = f2::pack(float(e0.f), float(e1.f));
   const float col_thr = (coord_exact8(e0.f) && coord_exact8(e1.f)) ? 0.5f : 0.5f - kNearTol;
-  const uint32_t bias = bias_reg();
+  const uint32_t bias = pin(bias_reg());
+  // shared addresses, computed once: ring slot 0 + this lane's tap words, the
+  // visit list, the row table, the copy destination
   const uint32_t base = pin(uint32_t(__cvta_generic_to_shared(ring)));
-  // tap word offsets (4-byte aligned) and funnel shifts of columns x / x + 1
-  const uint32_t a0 = S.ta[0] & ~3u, b0 = S.tb[0] & ~3u, a1 = S.ta[1] & ~3u, b1 = S.tb[1] & ~3u;
+  const uint32_t a0 = pin(base + (S.ta[0] & ~3u)), b0 = pin(base + (S.tb[0] & ~3u));
+  const uint32_t a1 = pin(base + (S.ta[1] & ~3u)), b1 = pin(base + (S.tb[1] & ~3u));
   const uint32_t sa0 = 8 * (S.ta[0] & 3u), sb0 = 8 * (S.tb[0] & 3u), sa1 = 8 * (S.ta[1] & 3u),
                  sb1 = 8 * (S.tb[1] & 3u);
+  const uint32_t cdst = pin(base + S.dst);
+  uint32_t vp = pin(uint32_t(__cvta_generic_to_shared(V.v)));
+  uint32_t qp = pin(uint32_t(__cvta_generic_to_shared(R.q)));
   using Cur = typename std::conditional<VEC, VecOut, PairOut<NL, OLK, SPLIT>>::type;
   Cur out(w, x, y0, swap);
   const uint32_t nv = V.n;
-  const uint32_t cdst = base + S.dst;
   // prologue: visits 0 .. kRing - 2 in flight (one commit group per visit)
 #pragma unroll
   for (uint32_t j = 0; j < kRing - 1; ++j) {
-    if (j < nv && S.n) cp_async16(cdst + j * kRingRow, at_row(S.g, visit_row(V.v[j]), S.pitch), S.n);
+    if (j < nv && S.n) cp_async16(cdst + j * kRingRow, at_row(S.g, visit_row(lds32(vp + 4 * j)), S.pitch), S.n);
     cp_commit();
   }
   uint64_t hA[3] = {0, 0, 0}, hB[3] = {0, 0, 0};
   uint32_t k = 0;
-  auto visit = [&](uint32_t i, uint64_t (&cur)[3], const uint64_t (&prev)[3]) {
+  // visit i = i0 + U (ring slot U, compile-time): H-lerp its row into `cur`,
+  // start the copy of visit i + kRing - 1, emit the output rows it completes
+  auto visit = [&](auto U, uint32_t i, uint64_t (&cur)[3], const uint64_t (&prev)[3]) {
+    constexpr uint32_t u = decltype(U)::value;
+    constexpr uint32_t slot = u * kRingRow, aslot = ((u + kRing - 1) % kRing) * kRingRow;
     cp_wait<kRing - 2>();  // visit i's row has landed (this lane's chunk) ...
     __syncwarp();           // ... and every lane's; every lane is also done with visit i - 1's slot
-    const uint32_t ahead = i + kRing - 1;
-    if (ahead < nv && S.n)
-      cp_async16(cdst + (ahead % kRing) * kRingRow, at_row(S.g, visit_row(V.v[ahead]), S.pitch), S.n);
+    if (i + kRing - 1 < nv && S.n)
+      cp_async16(cdst + aslot, at_row(S.g, visit_row(lds32(vp + 4 * (u + kRing - 1))), S.pitch), S.n);
     cp_commit();
-    const uint32_t rb = base + (i % kRing) * kRingRow;
-    const uint32_t ta0 = __funnelshift_r(lds32(rb + a0), lds32(rb + a0 + 4), sa0);
-    const uint32_t tb0 = __funnelshift_r(lds32(rb + b0), lds32(rb + b0 + 4), sb0);
-    const uint32_t ta1 = __funnelshift_r(lds32(rb + a1), lds32(rb + a1 + 4), sa1);
-    const uint32_t tb1 = __funnelshift_r(lds32(rb + b1), lds32(rb + b1 + 4), sb1);
+    const uint32_t ta0 = __funnelshift_r(lds32(a0 + slot), lds32(a0 + slot + 4), sa0);
+    const uint32_t tb0 = __funnelshift_r(lds32(b0 + slot), lds32(b0 + slot + 4), sb0);
+    const uint32_t ta1 = __funnelshift_r(lds32(a1 + slot), lds32(a1 + slot + 4), sa1);
+    const uint32_t tb1 = __funnelshift_r(lds32(b1 + slot), lds32(b1 + slot + 4), sb1);
     hlerp2<NL>(ta0, tb0, ta1, tb1, fx, bias, cur);
-    const uint32_t end = visit_end(V.v[i]);
+    const uint32_t end = visit_end(lds32(vp + 4 * u));
     if (active) {
 #pragma unroll 1
-      for (; k < end; ++k)
-        emit2<NL, OLK, SPLIT, SIG, VEC, Out>(prev, cur, R.q[k], k, col_thr, ks, lut, swap, col1, al, out, fix);
+      for (; k < end; ++k, qp += 8) {
+        float2 q;
+        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(q.x), "=f"(q.y) : "r"(qp));
+        emit2<NL, OLK, SPLIT, SIG, VEC, Out>(prev, cur, q, k, col_thr, ks, lut, swap, col1, al, out, fix);
+      }
     }
   };
-  for (uint32_t i = 0; i < nv; i += 2) {
-    visit(i, hA, hB);
-    if (i + 1 < nv) visit(i + 1, hB, hA);
+  for (uint32_t i0 = 0; i0 < nv; i0 += kRing, vp += 4 * kRing) {
+    static_assert(kRing == 4 || kRing == 8, "the walk is unrolled by the ring size");
+    visit(std::integral_constant<uint32_t, 0>(), i0, hA, hB);
+    if (i0 + 1 >= nv) break;
+    visit(std::integral_constant<uint32_t, 1>(), i0 + 1, hB, hA);
+    if (i0 + 2 >= nv) break;
+    visit(std::integral_constant<uint32_t, 2>(), i0 + 2, hA, hB);
+    if (i0 + 3 >= nv) break;
+    visit(std::integral_constant<uint32_t, 3>(), i0 + 3, hB, hA);
+    if (kRing == 4 || i0 + 4 >= nv) continue;
+    visit(std::integral_constant<uint32_t, 4 % kRing>(), i0 + 4, hA, hB);
+    if (i0 + 5 >= nv) break;
+    visit(std::integral_constant<uint32_t, 5 % kRing>(), i0 + 5, hB, hA);
+    if (i0 + 6 >= nv) break;
+    visit(std::integral_constant<uint32_t, 6 % kRing>(), i0 + 6, hA, hB);
+    if (i0 + 7 >= nv) break;
+    visit(std::integral_constant<uint32_t, 7 % kRing>(), i0 + 7, hB, hA);
   }
   cp_wait<0>();
 }
@@ -845,10 +894,10 @@ __global__ void __launch_bounds__(32, FK_SEP_MINB) fk_resample_sep(const __grid_
           // slots share their lane swap, so `swap` is warp-uniform
           if (AFFINE && P.aff_inline && !swap) {
             pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring, S, e0, e1, active, x, col1, y_begin,
-                                                                 swap, al, KPar<NL, false>{P}, my_lut, fix);
+                                                                 swap, al, KPin<NL, SIG, false>(P), my_lut, fix);
           } else if (AFFINE && P.aff_inline) {
             pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring, S, e0, e1, active, x, col1, y_begin,
-                                                                 swap, al, KPar<NL, true>{P}, my_lut, fix);
+                                                                 swap, al, KPin<NL, SIG, true>(P), my_lut, fix);
           } else {
             AffConsts K;
             if constexpr (AFFINE) load_affine<NL, SIG>(P, z, swap, K);
