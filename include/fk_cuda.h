@@ -13,6 +13,9 @@ extern "C" {
 int32_t fk_cuda_device_info(char* buf, size_t cap);
 /* Fused-kernel launches enqueued by this process so far (all executors). */
 uint64_t fk_cuda_kernel_launch_count(void);
+/* Name of the kernel the last fused execute on this thread launched
+   ("fk_direct", "fk_resample_sep", "fk_resample", "fk_transform_generic"), or "". */
+const char* fk_cuda_last_kernel(void);
 
 #ifdef __cplusplus
 }

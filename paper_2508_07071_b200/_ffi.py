@@ -139,6 +139,7 @@ SIGNATURES = {
 CUDA_SIGNATURES = {
     "fk_cuda_device_info": (I32, [C.c_char_p, C.c_size_t]),
     "fk_cuda_kernel_launch_count": (C.c_uint64, []),
+    "fk_cuda_last_kernel": (C.c_char_p, []),
 }
 
 _loaded: dict[str, C.CDLL] = {}

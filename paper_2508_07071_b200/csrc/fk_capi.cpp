@@ -235,5 +235,6 @@ int32_t fk_cuda_device_info(char* buf, size_t cap) {
   return FK_OK;
 }
 uint64_t fk_cuda_kernel_launch_count(void) { return fk::launch_count(); }
+const char* fk_cuda_last_kernel(void) { return fk::last_kernel(); }
 
 }  // extern "C"

@@ -27,7 +27,19 @@ namespace fk {
 
 namespace {
 
-constexpr int kD = 16;  // elements per thread
+#ifndef FK_DIRECT_D
+#define FK_DIRECT_D 16
+#endif
+constexpr int kD = FK_DIRECT_D;  // elements per thread (kD / 4 chunks of 4)
+constexpr int kChunks = kD / 4;
+#ifndef FK_DIRECT_TILES
+#define FK_DIRECT_TILES 1
+#endif
+#ifndef FK_DIRECT_MINB
+#define FK_DIRECT_MINB 6
+#endif
+constexpr int kTilesPerIter = FK_DIRECT_TILES;  // warp tiles loaded before any is computed
+constexpr int kDirectMinBlocks = FK_DIRECT_MINB;
 
 // registered chains; bit 12+k marks op k as a verified reciprocal division
 #define FK_DIRECT_SIGS(X)                                                                         \
@@ -35,7 +47,9 @@ constexpr int kD = 16;  // elements per thread
   X(sig_make(1, AF_DIV)) X(sig_make(1, AF_DIV, 0, 0, 0, 1)) X(sig_make(2, AF_MUL, AF_ADD))          \
   X(sig_make(2, AF_SUB, AF_DIV)) X(sig_make(2, AF_SUB, AF_DIV, 0, 0, 2))                            \
   X(sig_make(3, AF_MUL, AF_SUB, AF_DIV)) X(sig_make(3, AF_MUL, AF_SUB, AF_DIV, 0, 4))               \
-  X(sig_make(4, AF_MUL, AF_ADD, AF_SUB, AF_DIV)) X(sig_make(4, AF_MUL, AF_ADD, AF_SUB, AF_DIV, 8))
+  X(sig_make(4, AF_MUL, AF_ADD, AF_SUB, AF_DIV)) X(sig_make(4, AF_MUL, AF_ADD, AF_SUB, AF_DIV, 8))               \
+  X(sig_make(1, AF_DIV, 0, 0, 0, 1, 1)) X(sig_make(2, AF_SUB, AF_DIV, 0, 0, 2, 2))                          \
+  X(sig_make(3, AF_MUL, AF_SUB, AF_DIV, 0, 4, 4)) X(sig_make(4, AF_MUL, AF_ADD, AF_SUB, AF_DIV, 8, 8))
 
 template <uint32_t SIG, int K>
 __device__ __forceinline__ float direct_elem(float v, float c, float r) {
@@ -43,10 +57,53 @@ __device__ __forceinline__ float direct_elem(float v, float c, float r) {
   else return sig_op<SIG, K>(v, c, r);
 }
 
+// Packed FP32 (FFMA2 / FMUL2 / FADD2, sm_100): two elements per instruction,
+// each an IEEE round-to-nearest operation exactly like its scalar form.
+#ifndef FK_DIRECT_FP2
+#define FK_DIRECT_FP2 0
+#endif
+namespace p2 {
+__device__ __forceinline__ uint64_t pk(float lo, float hi) {
+  uint64_t d;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(d) : "f"(lo), "f"(hi));
+  return d;
+}
+__device__ __forceinline__ void up(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+template <uint32_t FN>
+__device__ __forceinline__ uint64_t op(uint64_t a, uint64_t b) {
+  uint64_t d;
+  if constexpr (FN == AF_MUL) asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  else if constexpr (FN == AF_ADD) asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  else asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+}  // namespace p2
+
 template <uint32_t SIG, int K>
 __device__ __forceinline__ void direct_op(float (&v)[kD], float c, float r, uint32_t reps) {
-  if constexpr (K < sig_n(SIG)) {
-    if constexpr (sig_fn(SIG, K) == AF_DIV && sig_fast(SIG, K)) {
+  if constexpr (K < sig_n(SIG) && sig_fn(SIG, K) != AF_DIV && FK_DIRECT_FP2) {
+    // Mul / Add / Sub: packed pairs
+    constexpr uint32_t FN = sig_fn(SIG, K);
+    uint64_t q[kD / 2];
+#pragma unroll
+    for (int e = 0; e < kD / 2; ++e) q[e] = p2::pk(v[2 * e], v[2 * e + 1]);
+    const uint64_t cc = p2::pk(c, c);
+#pragma unroll 1
+    for (uint32_t i = 0; i < reps; ++i)
+#pragma unroll
+      for (int e = 0; e < kD / 2; ++e) q[e] = p2::op<FN>(q[e], cc);
+#pragma unroll
+    for (int e = 0; e < kD / 2; ++e) p2::up(q[e], v[2 * e], v[2 * e + 1]);
+  } else if constexpr (K < sig_n(SIG)) {
+    if constexpr (sig_fn(SIG, K) == AF_DIV && sig_total(SIG, K)) {
+      // the reciprocal form was proven exact on all 2^32 inputs for this divisor
+#pragma unroll 1
+      for (uint32_t i = 0; i < reps; ++i)
+#pragma unroll
+        for (int e = 0; e < kD; ++e) v[e] = div_by_recip(v[e], c, r);
+    } else if constexpr (sig_fn(SIG, K) == AF_DIV && sig_fast(SIG, K)) {
       // div_guarded for the whole tile: reciprocal form everywhere, then (rarely)
       // IEEE division for the elements outside its verified range
 #pragma unroll 1
@@ -94,11 +151,25 @@ __device__ __forceinline__ TileAt tile_at(const DPlan& P, uint32_t t) {
   return TileAt{y, (t - y * P.tiles_per_row) * kWarpTile};
 }
 
+// A whole warp tile inside the row, with 16-byte aligned source chunks: no
+// per-chunk bounds or alignment checks (the common case).
+__device__ __forceinline__ bool tile_full(const DPlan& P, const DSample& s, TileAt at) {
+  return at.x0 + kWarpTile <= P.width && ((s.src + uint64_t(s.y0 + at.y) * s.pitch + uint64_t(s.x0) * 4) & 15) == 0;
+}
+
 __device__ __forceinline__ void load_tile(const DPlan& P, const DSample& s, TileAt at, uint32_t lane, float (&v)[kD]) {
   const float* row = reinterpret_cast<const float*>(reinterpret_cast<const uint8_t*>(s.src) +
                                                     uint64_t(s.y0 + at.y) * s.pitch) + s.x0;
+  if (tile_full(P, s, at)) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kChunks; ++i) {
+      const float4 q = __ldg(reinterpret_cast<const float4*>(row + at.x0 + 128u * i + 4u * lane));
+      v[4 * i] = q.x; v[4 * i + 1] = q.y; v[4 * i + 2] = q.z; v[4 * i + 3] = q.w;
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < kChunks; ++i) {
     const uint32_t x = at.x0 + 128u * i + 4u * lane;
     const float* p = row + x;
     if (x + 4 <= P.width && (reinterpret_cast<uintptr_t>(p) & 15) == 0) {
@@ -120,8 +191,28 @@ __device__ __forceinline__ void finish_tile(const DPlan& P, const DWrite& w, Til
   direct_op<SIG, 2>(v, c[2], r[2], rep[2]);
   direct_op<SIG, 3>(v, c[3], r[3], rep[3]);
   uint8_t* row = reinterpret_cast<uint8_t*>(w.dst[0]) + uint64_t(at.y) * w.pitch[0];
+  const uint32_t ob = TO_U8 ? 1u : 4u;
+  if (at.x0 + kWarpTile <= P.width && ((reinterpret_cast<uintptr_t>(row) + uint64_t(at.x0) * ob) & (4 * ob - 1)) == 0) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+    for (int i = 0; i < kChunks; ++i) {  // whole tile in the row, aligned: no per-chunk checks
+      const uint32_t x = at.x0 + 128u * i + 4u * lane;
+      if constexpr (TO_U8) {
+        uint32_t b[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) b[e] = f32_to_u8(v[4 * i + e]);
+        const uint32_t word = __byte_perm(__byte_perm(b[0], b[1], 0x0040), __byte_perm(b[2], b[3], 0x0040), 0x5410);
+        if (st) __stcs(reinterpret_cast<uint32_t*>(row + x), word);
+        else *reinterpret_cast<uint32_t*>(row + x) = word;
+      } else {
+        const float4 o = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        if (st) __stcs(reinterpret_cast<float4*>(reinterpret_cast<float*>(row) + x), o);
+        else *reinterpret_cast<float4*>(reinterpret_cast<float*>(row) + x) = o;
+      }
+    }
+    return;
+  }
+#pragma unroll
+  for (int i = 0; i < kChunks; ++i) {
     const uint32_t x = at.x0 + 128u * i + 4u * lane;
     if constexpr (TO_U8) {  // Cast f32 -> u8, then one 32-bit store per chunk
       uint32_t b[4];
@@ -154,7 +245,7 @@ __device__ __forceinline__ void finish_tile(const DPlan& P, const DWrite& w, Til
 // tail wave); two tiles in flight per warp: both tiles' loads are issued before
 // either is computed.
 template <uint32_t SIG, bool TO_U8>
-__global__ void __launch_bounds__(kBlock, 3) fk_direct(const __grid_constant__ DPlan P) {
+__global__ void __launch_bounds__(kBlock, kDirectMinBlocks) fk_direct(const __grid_constant__ DPlan P) {
   float c[4] = {0.f, 0.f, 0.f, 0.f}, r[4] = {0.f, 0.f, 0.f, 0.f};
   uint32_t rep[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -173,39 +264,46 @@ __global__ void __launch_bounds__(kBlock, 3) fk_direct(const __grid_constant__ D
     const DSample s = P.reads[z];
     const DWrite w = P.writes[z];
     if (!(w.flags & WF_ACTIVE)) continue;
-    for (uint32_t t = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); t < P.tiles; t += 2 * warps) {
-      const uint32_t t2 = t + warps;
-      float va[kD], vb[kD];
+    for (uint32_t t = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); t < P.tiles; t += kTilesPerIter * warps) {
+      float va[kD];
       const TileAt a = tile_at(P, t);
       load_tile(P, s, a, lane, va);
-      TileAt b{0, 0};
-      if (t2 < P.tiles) {
-        b = tile_at(P, t2);
-        load_tile(P, s, b, lane, vb);
+      if constexpr (kTilesPerIter == 2) {
+        const uint32_t t2 = t + warps;
+        float vb[kD];
+        TileAt b{0, 0};
+        if (t2 < P.tiles) {
+          b = tile_at(P, t2);
+          load_tile(P, s, b, lane, vb);
+        }
+        finish_tile<SIG, TO_U8>(P, w, a, lane, va, c, r, rep);
+        if (t2 < P.tiles) finish_tile<SIG, TO_U8>(P, w, b, lane, vb, c, r, rep);
+      } else {
+        finish_tile<SIG, TO_U8>(P, w, a, lane, va, c, r, rep);
       }
-      finish_tile<SIG, TO_U8>(P, w, a, lane, va, c, r, rep);
-      if (t2 < P.tiles) finish_tile<SIG, TO_U8>(P, w, b, lane, vb, c, r, rep);
     }
   }
 }
 
-// Exhaustive proof for one divisor: div_guarded(x, d, RN(1/d)) == __fdiv_rn(x, d)
-// for every one of the 2^32 f32 bit patterns x (NaN results compare equal).
+// Exhaustive proof for one divisor over every one of the 2^32 f32 bit patterns x
+// (NaN results compare equal): bit 0 of *bad = div_guarded(x, d, RN(1/d)) differs
+// from __fdiv_rn(x, d) somewhere, bit 1 = the unguarded div_by_recip does.
 __global__ void fk_verify_recip_div(float d, unsigned int* bad) {
   const float r = __frcp_rn(d);
   const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
   unsigned int found = 0;
   for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < (uint64_t(1) << 32); i += stride) {
     const float x = __uint_as_float(uint32_t(i));
-    const float a = div_guarded(x, d, r), b = __fdiv_rn(x, d);
-    if (__float_as_uint(a) != __float_as_uint(b) && !(isnan(a) && isnan(b))) found = 1;
+    const float a = div_guarded(x, d, r), b = __fdiv_rn(x, d), u = div_by_recip(x, d, r);
+    if (__float_as_uint(a) != __float_as_uint(b) && !(isnan(a) && isnan(b))) found |= 1u;
+    if (__float_as_uint(u) != __float_as_uint(b) && !(isnan(u) && isnan(b))) found |= 2u;
   }
-  if (found) atomicOr(bad, 1u);
+  if (found) atomicOr(bad, found);
 }
 
-bool recip_div_verified(float d) {
+int recip_div_verified(float d) {
   static std::mutex mu;
-  static std::map<uint32_t, bool> cache;
+  static std::map<uint32_t, int> cache;
   uint32_t key;
   std::memcpy(&key, &d, 4);
   {
@@ -214,12 +312,12 @@ bool recip_div_verified(float d) {
     if (it != cache.end()) return it->second;
   }
   unsigned int* flag = nullptr;
-  bool ok = false;
+  int ok = 0;
   if (cudaMalloc(&flag, sizeof(unsigned int)) == cudaSuccess) {
     cudaMemset(flag, 0, sizeof(unsigned int));
     fk_verify_recip_div<<<148 * 16, 256>>>(d, flag);
-    unsigned int h = 1;
-    if (cudaMemcpy(&h, flag, sizeof h, cudaMemcpyDeviceToHost) == cudaSuccess) ok = h == 0;
+    unsigned int h = 3;
+    if (cudaMemcpy(&h, flag, sizeof h, cudaMemcpyDeviceToHost) == cudaSuccess) ok = (h & 1u) ? 0 : ((h & 2u) ? 1 : 2);
     cudaFree(flag);
   }
   cudaGetLastError();
@@ -237,10 +335,13 @@ bool direct_registered(uint32_t sig) {
   return false;
 }
 
-// CTAs per plane: enough to fill every SM at full occupancy (two tiles per thread), no more.
+// CTAs per plane: one loop iteration (two warp tiles) per warp, so every load of
+// the plane is issued in the first wave that has room for it (a small plane is
+// latency-bound: a grid-stride loop would serialise its DRAM round trips); capped
+// at 16 waves of resident CTAs for very large planes.
 template <class K>
 uint32_t direct_grid_x(K kernel, uint32_t tiles, uint32_t planes) {
-  static int resident = 0;  // CTAs per SM, queried once per instantiation
+  static int resident = 0;  // CTAs per SM x SMs, queried once per instantiation
   if (!resident) {
     int dev = 0, sms = 0, occ = 0;
     cudaGetDevice(&dev);
@@ -248,9 +349,10 @@ uint32_t direct_grid_x(K kernel, uint32_t tiles, uint32_t planes) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kBlock, 0);
     resident = (sms > 0 ? sms : 148) * (occ > 0 ? occ : 1);
   }
-  const uint64_t want = (uint64_t(tiles) + 2 * (kBlock / 32) - 1) / (2 * (kBlock / 32));  // two warp tiles per warp
-  const uint64_t per_plane = (uint64_t(resident) + planes - 1) / planes;
-  return uint32_t(want < per_plane ? (want > 0 ? want : 1) : (per_plane > 0 ? per_plane : 1));
+  const uint64_t per_cta = uint64_t(kTilesPerIter) * (kBlock / 32);  // one loop iteration per warp
+  const uint64_t want = (uint64_t(tiles) + per_cta - 1) / per_cta;
+  const uint64_t cap = (16ull * uint64_t(resident) + planes - 1) / planes;
+  return uint32_t(want < cap ? (want > 0 ? want : 1) : (cap > 0 ? cap : 1));
 }
 
 cudaError_t launch_direct(uint32_t sig, bool to_u8, const DPlan& P, cudaStream_t st) {

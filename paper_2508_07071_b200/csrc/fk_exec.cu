@@ -25,6 +25,7 @@
 namespace fk {
 
 namespace {
+thread_local const char* t_last_kernel = "";  // kernel family of this thread's last fused execute
 
 std::atomic<uint64_t> g_launches{0};
 
@@ -490,12 +491,17 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
     }
     ok = ok && arith.size() <= 4 && uint32_t(p.write.in_kind) == (to_u8 ? FK_U8 : FK_F32);
     if (ok) {
-      uint32_t fn[4] = {0, 0, 0, 0}, fast = 0;
+      uint32_t fn[4] = {0, 0, 0, 0}, fast = 0, total = 0;
       for (size_t k = 0; k < arith.size(); ++k) {
         fn[k] = arith[k].fn;
-        if (fn[k] == AF_DIV && recip_div_verified(f32_bits(arith[k].c[0]))) fast |= 1u << k;
+        if (fn[k] == AF_DIV) {
+          const int lvl = recip_div_verified(f32_bits(arith[k].c[0]));
+          if (lvl >= 1) fast |= 1u << k;
+          if (lvl >= 2) total |= 1u << k;
+        }
       }
-      uint32_t sig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast);
+      uint32_t sig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast, total);
+      if (!direct_registered(sig)) sig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast);
       if (!direct_registered(sig)) sig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], 0);
       ok = direct_registered(sig);
       if (ok) {
@@ -753,6 +759,7 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
   P.writes = dp.d_writes;
   if (direct) {
     cuda_check(launch_direct(dp.dir_sig, dp.direct_u8, P, st), "fk_direct launch");
+    t_last_kernel = "fk_direct";
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     r.path = FK_PATH_COMPILED;
@@ -797,6 +804,7 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
     cuda_check(launch_resample_sep(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)), P.write_mode == WR_SPLIT,
                                    affine ? dp.aff_sig : kSigLut, S, stage_ok == 1 && !S.no_stage, st),
                "fk_resample_sep launch");
+    t_last_kernel = "fk_resample_sep";
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     r.path = FK_PATH_COMPILED;
@@ -804,11 +812,13 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
     cuda_check(launch_resample(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)), P.write_mode == WR_SPLIT,
                                affine ? dp.aff_sig : kSigLut, P, st),
                "fk_resample launch");
+    t_last_kernel = "fk_resample";
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     r.path = FK_PATH_COMPILED;
   } else {
     launch(cls, P, st, r.kernels_launched);
+    t_last_kernel = "fk_transform_generic";
     r.path = FK_PATH_GENERIC;
   }
   r.device_ms = timer.stop();
@@ -916,6 +926,8 @@ fk_exec_report execute_unfused(const Pipeline& p, const fk_exec_config* cfg) {
 }
 
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+const char* last_kernel() { return t_last_kernel; }
 
 std::string device_info() {
   int n = 0;

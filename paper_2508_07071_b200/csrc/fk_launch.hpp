@@ -21,7 +21,9 @@ int resample_elems();
 // compiled f32 element-wise chain kernel (fk_direct.cu)
 int direct_elems();
 bool direct_registered(uint32_t sig);
-bool recip_div_verified(float d);  // exhaustive 2^32-input device check, cached per divisor
+// exhaustive 2^32-input device check, cached per divisor: 0 = use IEEE division,
+// 1 = the guarded reciprocal form is exact, 2 = the unguarded one is too
+int recip_div_verified(float d);
 cudaError_t launch_direct(uint32_t sig, bool to_u8, const DPlan& P, cudaStream_t st);
 
 // compiled column-streaming u8 resample kernel (fk_resample_sep.cu); P.tiles_per_cta = band rows

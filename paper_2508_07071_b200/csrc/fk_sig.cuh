@@ -17,12 +17,14 @@ namespace fk {
 constexpr uint32_t kSigLut = 0xffffffffu;  // not a straight-line chain: tabulate (LUT mode)
 
 __host__ __device__ constexpr uint32_t sig_make(int n, uint32_t f0 = 0, uint32_t f1 = 0, uint32_t f2 = 0, uint32_t f3 = 0,
-                            uint32_t fast = 0) {
-  return uint32_t(n) | (f0 << 4) | (f1 << 6) | (f2 << 8) | (f3 << 10) | (fast << 12);
+                            uint32_t fast = 0, uint32_t total = 0) {
+  return uint32_t(n) | (f0 << 4) | (f1 << 6) | (f2 << 8) | (f3 << 10) | (fast << 12) | (total << 16);
 }
 __host__ __device__ constexpr int sig_n(uint32_t s) { return int(s & 0xfu); }
 __host__ __device__ constexpr uint32_t sig_fn(uint32_t s, int k) { return (s >> (4 + 2 * k)) & 3u; }
 __host__ __device__ constexpr bool sig_fast(uint32_t s, int k) { return (s >> (12 + k)) & 1u; }
+// bit 16+k: the reciprocal form is exact for EVERY f32 input of op k (no range guard)
+__host__ __device__ constexpr bool sig_total(uint32_t s, int k) { return (s >> (16 + k)) & 1u; }
 
 // Correctly rounded x / d from r = RN(1/d): q = RN(x r), e = x - q d (exact via
 // FMA), q' = RN(q + e r). Used only where the host has verified it equals

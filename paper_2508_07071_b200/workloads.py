@@ -36,6 +36,8 @@ class Workload:
     outputs: list = field(default_factory=list)   # torch storages written (for e2e D2H)
     keep: list = field(default_factory=list)
     info: dict = field(default_factory=dict)
+    rotate: list = field(default_factory=list)    # extra identical pipelines on their own planes
+                                                  # (timed steps cycle through them: sets > L2)
 
 
 def _touched_bilinear(lo: int, n: int, out: int) -> np.ndarray:
@@ -64,30 +66,41 @@ def unique_input_bytes(rects, frame_of, out_w, out_h, n_frames, fw=1920, fh=1080
     return int(masks.sum()) * bpe
 
 
-def c1(lib: Library, seed: int = 42, W: int = 3840, H: int = 2160) -> Workload:
+def c1(lib: Library, seed: int = 42, W: int = 3840, H: int = 2160, sets: int = 1) -> Workload:
+    """configs[0]; `sets` > 1 adds copies on their own planes (4 sets = 166 MB > L2)."""
     rng = np.random.default_rng(seed)
-    src = lib.plane_from_numpy(rng.random((H, W), dtype=np.float32))
-    dst = lib.plane_alloc(W, H, U8)
-    p = lib.validate_chain([lib.op_read_per_thread(src), lib.op_mul(f32(400.0)), lib.op_add(f32(2.0)),
-                            lib.op_sub(f32(1.5)), lib.op_div(f32(1.25)), lib.op_cast(F32, U8),
-                            lib.op_write_per_thread(dst)])
-    return Workload("C1", p, W * H, W * H * 5, W * H, W * H * 4, [src], [dst.storage], [src, dst],
-                    {"shape": f"{W}x{H}", "chain": "read f32 -> mul,add,sub,div -> cast u8 -> write"})
+    pipes, keep = [], []
+    for _ in range(sets):
+        src = lib.plane_from_numpy(rng.random((H, W), dtype=np.float32))
+        dst = lib.plane_alloc(W, H, U8)
+        pipes.append((lib.validate_chain([lib.op_read_per_thread(src), lib.op_mul(f32(400.0)), lib.op_add(f32(2.0)),
+                                          lib.op_sub(f32(1.5)), lib.op_div(f32(1.25)), lib.op_cast(F32, U8),
+                                          lib.op_write_per_thread(dst)]), src, dst))
+        keep += [src, dst]
+    p, src, dst = pipes[0]
+    return Workload("C1", p, W * H, W * H * 5, W * H, W * H * 4, [src], [dst.storage], keep,
+                    {"shape": f"{W}x{H}", "chain": "read f32 -> mul,add,sub,div -> cast u8 -> write"},
+                    [q for q, _, _ in pipes[1:]])
 
 
-def c3(lib: Library, n_ops: int, seed: int = 42, W: int = 4096, H: int = 4096) -> Workload:
+def c3(lib: Library, n_ops: int, seed: int = 42, W: int = 4096, H: int = 4096, sets: int = 1) -> Workload:
+    """configs[2]; `sets` > 1 adds copies on their own planes (2 sets = 268 MB > L2)."""
     rng = np.random.default_rng(seed)
-    src = lib.plane_from_numpy(rng.random((H, W), dtype=np.float32))
-    dst = lib.plane_alloc(W, H, F32)
-    chain = [lib.op_read_per_thread(src)]
-    for op, c, k in ((lib.op_mul, 1.0000001, (n_ops + 1) // 2), (lib.op_add, 1e-7, n_ops // 2)):
-        if k:  # bench.cpp:100-108: literal ops up to 64, a StaticLoop beyond
-            o = op(f32(c))
-            chain += [o] * k if k <= 64 else [lib.op_static_loop(o, k)]
-    chain.append(lib.op_write_per_thread(dst))
-    p = lib.validate_chain(chain)
-    return Workload(f"C3[N={n_ops}]", p, W * H, W * H * 8, W * H * 4, W * H * 4, [src], [dst.storage], [src, dst],
-                    {"shape": f"{W}x{H}", "n_ops": n_ops})
+    pipes, keep = [], []
+    for _ in range(sets):
+        src = lib.plane_from_numpy(rng.random((H, W), dtype=np.float32))
+        dst = lib.plane_alloc(W, H, F32)
+        chain = [lib.op_read_per_thread(src)]
+        for op, c, k in ((lib.op_mul, 1.0000001, (n_ops + 1) // 2), (lib.op_add, 1e-7, n_ops // 2)):
+            if k:  # bench.cpp:100-108: literal ops up to 64, a StaticLoop beyond
+                o = op(f32(c))
+                chain += [o] * k if k <= 64 else [lib.op_static_loop(o, k)]
+        chain.append(lib.op_write_per_thread(dst))
+        pipes.append((lib.validate_chain(chain), src, dst))
+        keep += [src, dst]
+    p, src, dst = pipes[0]
+    return Workload(f"C3[N={n_ops}]", p, W * H, W * H * 8, W * H * 4, W * H * 4, [src], [dst.storage], keep,
+                    {"shape": f"{W}x{H}", "n_ops": n_ops}, [q for q, _, _ in pipes[1:]])
 
 
 def crops_pipeline(lib: Library, frames: list, rects: list, frame_of, out_w: int, out_h: int,
