@@ -120,8 +120,16 @@ __device__ __forceinline__ void direct_op(float (&v)[kD], float c, float r, uint
         }
       }
     } else {
+      // StaticLoop / repeated literal ops: 4 repetitions per loop trip
+      uint32_t i = 0;
 #pragma unroll 1
-      for (uint32_t i = 0; i < reps; ++i)
+      for (; i + 4 <= reps; i += 4)
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int e = 0; e < kD; ++e) v[e] = direct_elem<SIG, K>(v[e], c, r);
+#pragma unroll 1
+      for (; i < reps; ++i)
 #pragma unroll
         for (int e = 0; e < kD; ++e) v[e] = direct_elem<SIG, K>(v[e], c, r);
     }
@@ -246,17 +254,10 @@ __device__ __forceinline__ void finish_tile(const DPlan& P, const DWrite& w, Til
 // either is computed.
 template <uint32_t SIG, bool TO_U8>
 __global__ void __launch_bounds__(kBlock, kDirectMinBlocks) fk_direct(const __grid_constant__ DPlan P) {
-  float c[4] = {0.f, 0.f, 0.f, 0.f}, r[4] = {0.f, 0.f, 0.f, 0.f};
-  uint32_t rep[4] = {0, 0, 0, 0};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (k < sig_n(SIG)) {
-      const DOp op = dev::prog_op(P, P.op_base + k);
-      c[k] = __uint_as_float(uint32_t(op.c[0]));
-      r[k] = __frcp_rn(c[k]);
-      rep[k] = op.repeat;
-    }
-  }
+  // chain constants at fixed kernel-parameter offsets (constant-bank operands)
+  const float c[4] = {P.aff_c[0][0], P.aff_c[1][0], P.aff_c[2][0], P.aff_c[3][0]};
+  const float r[4] = {P.aff_r[0][0], P.aff_r[1][0], P.aff_r[2][0], P.aff_r[3][0]};
+  const uint32_t rep[4] = {P.dir_rep[0], P.dir_rep[1], P.dir_rep[2], P.dir_rep[3]};
   const uint32_t lane = threadIdx.x & 31u;
   const uint32_t warps = gridDim.x * (kBlock / 32);
   for (uint32_t zi = blockIdx.z; zi < P.batch; zi += gridDim.z) {

@@ -758,6 +758,15 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
   P.reads = dp.d_reads;
   P.writes = dp.d_writes;
   if (direct) {
+    // the chain's constants at fixed parameter offsets: the kernel's FMUL/FADD
+    // read them as constant-bank operands
+    for (uint32_t k = 0; k < 4 && k < uint32_t(sig_n(dp.dir_sig)); ++k) {
+      const DOp& d = dp.table[dp.dir_base + k];
+      const float c = f32_bits(d.c[0]);
+      P.aff_c[k][0] = c;
+      P.aff_r[k][0] = 1.0f / c;  // RN(1/c) on the host: the same value as the device's __frcp_rn
+      P.dir_rep[k] = d.repeat;
+    }
     cuda_check(launch_direct(dp.dir_sig, dp.direct_u8, P, st), "fk_direct launch");
     t_last_kernel = "fk_direct";
     ++r.kernels_launched;

@@ -102,7 +102,7 @@ def main():
     path = os.path.join(ROOT, "profiles", f"ncu_summary_{rnd}.json")
     summary = json.load(open(path)) if os.path.exists(path) else {}
     for item in items:
-        w, rep = item.split("=", 1)
+        w, rep = item.rsplit("=", 1)
         s = summarise(rep, PX.get(w.split("[")[0]))
         summary[w] = s
         with open(os.path.join(ROOT, "profiles", f"ncu_{rnd}_{w}.txt"), "w") as f:
