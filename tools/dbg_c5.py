@@ -15,10 +15,14 @@ rects = []
 for _ in range(int(sys.argv[1]) if len(sys.argv) > 1 else 4):
     w, h = int(r.integers(112, 449)), int(r.integers(112, 449))
     rects.append((int(r.integers(0, 1921 - w)), int(r.integers(0, 1081 - h)), w, h))
-spec = batch_spec(frames, rects, 224, 224, post=[], compute=[], write=U8X3, split=False)
+if os.environ.get("DBG_AFFINE"):
+    spec = batch_spec(frames, rects, 224, 224, post=[("cast", U8X3, F32X3)])
+else:
+    spec = batch_spec(frames, rects, 224, 224, post=[], compute=[], write=U8X3, split=False)
 a, _ = run(cuda, spec); b, _ = run(oracle, spec)
 for z, (da, db) in enumerate(zip(a, b)):
-    x, y = da[0].astype(int), db[0].astype(int)
+    x, y = np.stack(da, -1) if len(da) > 1 else da[0], np.stack(db, -1) if len(db) > 1 else db[0]
+    x, y = x.view(np.int32) if x.dtype == np.float32 else x.astype(int), y.view(np.int32) if y.dtype == np.float32 else y.astype(int)
     bad = np.argwhere(np.any(x != y, axis=-1) if x.ndim == 3 else x != y)
     print("z", z, rects[z], "shape", x.shape, "bad px", len(bad))
     if len(bad):
