@@ -176,6 +176,23 @@ fk_status fk_plan_memory_savings(const fk_pipeline* p, uint64_t* bytes);        
 fk_status fk_schedule(const fk_extent3* space, const fk_exec_config* cfg, uint32_t* tasks,
                       uint64_t cap, uint64_t* count);
 
+/* ---- ReduceDPP (dpp.hpp:32-53, dpp.cpp:46-246) ----------------------------- */
+enum fk_reducer { FK_REDUCE_SUM = 0, FK_REDUCE_MAX = 1, FK_REDUCE_MIN = 2 }; /* Reducer, dpp.hpp:32 */
+typedef struct fk_reduce_spec {  /* ReduceSpec, dpp.hpp:37-41 */
+  const fk_iop* transform;       /* optional Unary/Binary compute IOp, NULL = identity */
+  uint32_t combine;              /* fk_reducer */
+  uint32_t has_identity;         /* 0: reducer_identity(combine, value kind), dpp.cpp:48-73 */
+  uint8_t identity[24];          /* Element bytes in the value kind */
+} fk_reduce_spec;
+/* multi_reduce_plane, dpp.hpp:52 / dpp.cpp:158-241: every spec folded over the
+   read's iteration space in ONE traversal of the source; results[s] = Element
+   bytes (24 each) in spec s's value kind; *elements_read = source elements read
+   (nullable). workers: the reference's partition (0 = hardware default); it
+   only changes float sums (double accumulation, agreement within 2^-20
+   relative). */
+fk_status fk_multi_reduce_plane(const fk_iop* read, const fk_reduce_spec* specs, uint32_t n, int32_t workers,
+                                void* results, uint64_t* elements_read);
+
 #ifdef __cplusplus
 }
 #endif

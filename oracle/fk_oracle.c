@@ -1042,3 +1042,150 @@ fk_status fk_plan_memory_savings(const fk_pipeline* p, uint64_t* bytes) { /* exe
   *bytes = b;
   return FK_OK;
 }
+
+/* ---------------------------------------------------------------- reduce -- */
+/* ReduceDPP, dpp.cpp:46-246. Sequential per-worker folds over contiguous row
+   ranges, partials merged in worker-index order; float sums in double. */
+
+static void reducer_identity(uint32_t r, uint32_t kind, elem_t* e) { /* dpp.cpp:48-73 */
+  const uint32_t lk = lane_kind(kind);
+  double v = 0.0;
+  if (r == FK_REDUCE_MAX) v = lk == FK_U8 ? 0.0 : -INFINITY;
+  else if (r == FK_REDUCE_MIN) v = lk == FK_U8 ? 255.0 : INFINITY;
+  memset(e, 0, sizeof *e);
+  for (int l = 0; l < lane_count(kind); ++l) {
+    switch (lk) {
+      case FK_U8: e->u8v[l] = (uint8_t)v; break;
+      case FK_F32: e->f32v[l] = (float)v; break;
+      default: e->f64v[l] = v; break;
+    }
+  }
+}
+
+/* combine_lane / combine_elements, dpp.cpp:77-106 */
+static void combine_elements(uint32_t r, uint32_t kind, elem_t* a, const elem_t* b) {
+  const uint32_t lk = lane_kind(kind);
+  for (int l = 0; l < lane_count(kind); ++l) {
+    switch (lk) {
+      case FK_U8: {
+        const uint8_t x = a->u8v[l], y = b->u8v[l];
+        a->u8v[l] = r == FK_REDUCE_SUM ? (uint8_t)(x + y) : r == FK_REDUCE_MAX ? (x < y ? y : x) : (y < x ? y : x);
+        break;
+      }
+      case FK_F32: {
+        const float x = a->f32v[l], y = b->f32v[l];
+        a->f32v[l] = r == FK_REDUCE_SUM ? x + y : r == FK_REDUCE_MAX ? (x < y ? y : x) : (y < x ? y : x);
+        break;
+      }
+      default: {
+        const double x = a->f64v[l], y = b->f64v[l];
+        a->f64v[l] = r == FK_REDUCE_SUM ? x + y : r == FK_REDUCE_MAX ? (x < y ? y : x) : (y < x ? y : x);
+        break;
+      }
+    }
+  }
+}
+
+typedef struct spec_accum { /* SpecAccum, dpp.cpp:116-127 */
+  int double_sum;
+  double d[3];
+  elem_t e;
+} spec_accum_t;
+
+static void make_accum(spec_accum_t* a, uint32_t r, uint32_t kind) {
+  memset(a, 0, sizeof *a);
+  a->double_sum = r == FK_REDUCE_SUM && lane_kind(kind) != FK_U8;
+  if (!a->double_sum) reducer_identity(r, kind, &a->e);
+}
+
+#define RED_BLOCK 64 /* kReduceBlock, dpp.cpp:110 */
+
+fk_status fk_multi_reduce_plane(const fk_iop* read, const fk_reduce_spec* specs, uint32_t n, int32_t workers,
+                                void* results, uint64_t* elements_read) {
+  /* multi_reduce_plane, dpp.cpp:158-241 */
+  if (!read || (n && (!specs || !results))) return fail(FK_E_INVALID_ARGUMENT, -1, "null argument");
+  if (n == 0) return fail(FK_E_EMPTY_ITER_SPACE, -1, "no reduce specs given");
+  if (read->opkind != FK_KIND_READ) return fail(FK_E_FIRST_NOT_READ, -1, "iteration space comes from a read op");
+  if (!read->has_dims) return fail(FK_E_MISSING_DIMS, -1, "%s has no dims hint", op_name(read->id));
+  const fk_extent3 sp = read->dims;
+  if ((uint64_t)sp.width * sp.height * sp.batch == 0) return fail(FK_E_EMPTY_ITER_SPACE, -1, "empty iteration space");
+  uint32_t* vkind = (uint32_t*)calloc(n, sizeof(uint32_t));
+  elem_t* ident = (elem_t*)calloc(n, sizeof(elem_t));
+  for (uint32_t s = 0; s < n; ++s) {
+    const fk_iop* t = specs[s].transform;
+    if (t) {
+      if (t->opkind != FK_KIND_UNARY && t->opkind != FK_KIND_BINARY) {
+        free(vkind); free(ident);
+        return fail(FK_E_INVALID_CONFIG, -1, "reduce transform must be a compute op");
+      }
+      if (t->in_kind != read->out_kind) {
+        free(vkind); free(ident);
+        return fail(FK_E_KIND_MISMATCH, -1, "reduce transform input kind vs read output");
+      }
+      vkind[s] = (uint32_t)(t->out_kind >= 0 ? t->out_kind : t->in_kind);
+    } else {
+      vkind[s] = (uint32_t)read->out_kind;
+    }
+    if (specs[s].has_identity) memcpy(&ident[s], specs[s].identity, sizeof(elem_t));
+    else reducer_identity(specs[s].combine, vkind[s], &ident[s]);
+  }
+  const int w_req = workers > 0 ? workers : omp_get_max_threads();
+  const uint64_t total_rows = (uint64_t)sp.height * sp.batch;
+  const int w_count = (int)((uint64_t)w_req < total_rows ? (uint64_t)w_req : total_rows);
+  spec_accum_t* part = (spec_accum_t*)calloc((size_t)w_count * n, sizeof(spec_accum_t));
+  uint64_t* reads = (uint64_t*)calloc((size_t)w_count, sizeof(uint64_t));
+#pragma omp parallel for schedule(static, 1) num_threads(w_count)
+  for (int w = 0; w < w_count; ++w) {
+    spec_accum_t* mine = part + (size_t)w * n;
+    for (uint32_t s = 0; s < n; ++s) make_accum(&mine[s], specs[s].combine, vkind[s]);
+    const uint64_t r0 = total_rows * (uint64_t)w / (uint64_t)w_count, r1 = total_rows * (uint64_t)(w + 1) / (uint64_t)w_count;
+    io_t io;
+    memset(&io, 0, sizeof io);
+    for (uint64_t row = r0; row < r1; ++row) {
+      const uint32_t z = (uint32_t)(row / sp.height);
+      const int64_t y = (int64_t)(row % sp.height);
+      for (uint32_t x = 0; x < sp.width; ++x) {
+        elem_t v;
+        memset(&v, 0, sizeof v);
+        read_exec(read, (int64_t)x, y, z, &v, &io);
+        for (uint32_t s = 0; s < n; ++s) {
+          elem_t t = v;
+          if (specs[s].transform) compute_apply(specs[s].transform, &t, z);
+          if (mine[s].double_sum) {
+            for (int l = 0; l < lane_count(vkind[s]); ++l) mine[s].d[l] += lane_as_double(vkind[s], &t, l);
+          } else {
+            combine_elements(specs[s].combine, vkind[s], &mine[s].e, &t);
+          }
+        }
+      }
+    }
+    reads[w] = io.elements_read;
+  }
+  uint64_t total_reads = 0;
+  for (int w = 0; w < w_count; ++w) total_reads += reads[w];
+  if (elements_read) *elements_read = total_reads;
+  for (uint32_t s = 0; s < n; ++s) { /* merge in worker-index order, finish_accum (dpp.cpp:138-152) */
+    spec_accum_t acc;
+    make_accum(&acc, specs[s].combine, vkind[s]);
+    if (!acc.double_sum) acc.e = ident[s];
+    for (int w = 0; w < w_count; ++w) {
+      const spec_accum_t* f = part + (size_t)w * n + s;
+      if (acc.double_sum) for (int l = 0; l < 3; ++l) acc.d[l] += f->d[l];
+      else combine_elements(specs[s].combine, vkind[s], &acc.e, &f->e);
+    }
+    elem_t out;
+    memset(&out, 0, sizeof out);
+    if (!acc.double_sum) {
+      out = acc.e;
+    } else {
+      for (int l = 0; l < lane_count(vkind[s]); ++l) {
+        const double total = lane_as_double(vkind[s], &ident[s], l) + acc.d[l];
+        if (lane_kind(vkind[s]) == FK_F32) out.f32v[l] = (float)total;
+        else out.f64v[l] = total;
+      }
+    }
+    memcpy((uint8_t*)results + 24 * (size_t)s, &out, 24);
+  }
+  free(vkind); free(ident); free(part); free(reads);
+  return FK_OK;
+}

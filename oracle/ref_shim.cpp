@@ -22,6 +22,7 @@
 #include <tuple>
 #include <vector>
 
+#include "opfuse/dpp.hpp"
 #include "opfuse/executor.hpp"
 #include "opfuse/oplib.hpp"
 #include "opfuse/ops.hpp"
@@ -389,3 +390,32 @@ fk_status fk_schedule(const fk_extent3* sp, const fk_exec_config* c, uint32_t* t
 }
 
 }  // extern "C"
+
+// multi_reduce_plane (dpp.cpp:158-241) over the reference; elements_read from
+// the reference's instrumented counter (stats::add_elements_read, dpp.cpp:229).
+extern "C" fk_status fk_multi_reduce_plane(const fk_iop* read, const fk_reduce_spec* specs, uint32_t n,
+                                           int32_t workers, void* results, uint64_t* elements_read) {
+  if (!read || (!specs && n) || (!results && n))
+    return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: null argument");
+  try {
+    for (auto& b : read->srcs) copy_in(*b);
+    std::vector<ReduceSpec> rs(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      if (specs[i].transform) rs[i].transform = specs[i].transform->op;
+      rs[i].combine = static_cast<Reducer>(specs[i].combine);
+      if (specs[i].has_identity) {
+        Element e;
+        std::memcpy(&e, specs[i].identity, sizeof e);
+        rs[i].identity = e;
+      }
+    }
+    const uint64_t before = stats::elements_read();
+    const std::vector<Element> out = multi_reduce_plane(read->op, rs, workers);
+    if (elements_read) *elements_read = stats::elements_read() - before;
+    for (uint32_t i = 0; i < n; ++i) std::memcpy(static_cast<uint8_t*>(results) + 24 * size_t(i), &out[i], 24);
+    return FK_OK;
+  } catch (const Error& e) {
+    return set_error(e);
+  }
+}
+

@@ -84,6 +84,11 @@ class fk_exec_config(C.Structure):
                 ("flags", C.c_uint32), ("stream", C.c_void_p)]
 
 
+class fk_reduce_spec(C.Structure):
+    _fields_ = [("transform", C.c_void_p), ("combine", C.c_uint32), ("has_identity", C.c_uint32),
+                ("identity", C.c_uint8 * 24)]
+
+
 class fk_exec_report(C.Structure):
     _fields_ = [("wall_time_ns", C.c_uint64), ("bytes_read", C.c_uint64), ("bytes_written", C.c_uint64),
                 ("intermediate_bytes_allocated", C.c_uint64), ("passes", C.c_uint64),
@@ -133,7 +138,10 @@ SIGNATURES = {
     "fk_plan_memory_savings": (I32, [P, C.POINTER(C.c_uint64)]),
     "fk_schedule": (I32, [C.POINTER(fk_extent3), C.POINTER(fk_exec_config), C.POINTER(C.c_uint32),
                           C.c_uint64, C.POINTER(C.c_uint64)]),
+    "fk_multi_reduce_plane": (I32, [P, C.POINTER(fk_reduce_spec), U32, I32, P, C.POINTER(C.c_uint64)]),
 }
+
+REDUCE_SUM, REDUCE_MAX, REDUCE_MIN = 0, 1, 2  # fk_reducer (dpp.hpp:32)
 
 # symbols only the CUDA product exports (declared in include/fk_cuda.h)
 CUDA_SIGNATURES = {

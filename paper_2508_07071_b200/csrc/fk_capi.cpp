@@ -237,4 +237,21 @@ int32_t fk_cuda_device_info(char* buf, size_t cap) {
 uint64_t fk_cuda_kernel_launch_count(void) { return fk::launch_count(); }
 const char* fk_cuda_last_kernel(void) { return fk::last_kernel(); }
 
+fk_status fk_multi_reduce_plane(const fk_iop* read, const fk_reduce_spec* specs, uint32_t n, int32_t workers,
+                                void* results, uint64_t* elements_read) {
+  return guard([&] {
+    const fk::Op& r = deref(read, "read op");
+    if (n && (!specs || !results)) fk::fail(FK_E_INVALID_ARGUMENT, "null specs / results");
+    std::vector<fk::ReduceSpecHost> hs(n);
+    for (uint32_t i = 0; i < n; ++i) {
+      hs[i].transform = specs[i].transform ? &specs[i].transform->op : nullptr;
+      hs[i].combine = specs[i].combine;
+      hs[i].has_identity = specs[i].has_identity != 0;
+      std::memcpy(hs[i].identity.raw, specs[i].identity, 24);
+    }
+    const std::vector<fk::Element> out = fk::multi_reduce(r, hs, workers, nullptr, elements_read);
+    for (uint32_t i = 0; i < n; ++i) std::memcpy(static_cast<uint8_t*>(results) + 24 * size_t(i), out[i].raw, 24);
+  });
+}
+
 }  // extern "C"

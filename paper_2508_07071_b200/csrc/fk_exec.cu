@@ -18,6 +18,7 @@
 #include <tuple>
 
 #include "fk_core.hpp"
+#include "fk_reduce.hpp"
 #include "fk_exec.hpp"
 #include "fk_launch.hpp"
 #include "fk_sig.cuh"
@@ -932,6 +933,136 @@ fk_exec_report execute_unfused(const Pipeline& p, const fk_exec_config* cfg) {
   r.points_visited = uint64_t(W) * H * B * r.passes;
   r.path = FK_PATH_GENERIC;
   return r;
+}
+
+// ----------------------------------------------------------- ReduceDPP --
+namespace {
+
+// reducer_identity, dpp.cpp:48-73, as lane bits of the value kind
+void reducer_identity_bits(uint32_t r, uint32_t kind, uint64_t (&out)[3]) {
+  const uint32_t lk = lane_kind(kind);
+  double v = 0.0;
+  if (r == FK_REDUCE_MAX) v = lk == FK_U8 ? 0.0 : -INFINITY;
+  else if (r == FK_REDUCE_MIN) v = lk == FK_U8 ? 255.0 : INFINITY;
+  for (int l = 0; l < 3; ++l) {
+    if (lk == FK_U8) out[l] = uint64_t(v);
+    else if (lk == FK_F32) {
+      const float f = float(v);
+      uint32_t b;
+      std::memcpy(&b, &f, 4);
+      out[l] = b;
+    } else {
+      std::memcpy(&out[l], &v, 8);
+    }
+  }
+}
+
+void element_bits(uint32_t kind, const Element& e, uint64_t (&out)[3], bool as_double) {
+  for (int l = 0; l < 3; ++l) {
+    out[l] = 0;
+    if (l >= lanes_of(kind)) continue;
+    if (as_double) {
+      const double d = lane_as_double(kind, e, l);
+      std::memcpy(&out[l], &d, 8);
+    } else {
+      std::memcpy(&out[l], e.raw + l * lane_bytes(kind), lane_bytes(kind));
+    }
+  }
+}
+
+}  // namespace
+
+std::vector<Element> multi_reduce(const Op& read, const std::vector<ReduceSpecHost>& specs, int workers,
+                                  cudaStream_t st, uint64_t* elements_read) {
+  (void)workers;  // the device fold's partition is its own; only float sums can tell (within 2^-20)
+  if (specs.empty()) fail(FK_E_EMPTY_ITER_SPACE, "no reduce specs given");
+  if (read.opkind != FK_KIND_READ) fail(FK_E_FIRST_NOT_READ, "iteration space comes from a read op");
+  if (!read.dims) fail(FK_E_MISSING_DIMS, std::string(op_name(read.id)) + " has no dims hint");
+  const fk_extent3 sp = *read.dims;
+  if (uint64_t(sp.width) * sp.height * sp.batch == 0) fail(FK_E_EMPTY_ITER_SPACE, "empty iteration space");
+  // the read and every transform as one device program (a chain never executed
+  // as such: its write is a placeholder), so the kernel reuses the fused read stage
+  Pipeline pl;
+  pl.read = read;
+  pl.space = sp;
+  std::vector<uint32_t> vkind(specs.size()), top(specs.size(), kNoOp);
+  for (size_t s = 0; s < specs.size(); ++s) {
+    const Op* t = specs[s].transform;
+    if (t) {
+      if (t->opkind != FK_KIND_UNARY && t->opkind != FK_KIND_BINARY)
+        fail(FK_E_INVALID_CONFIG, "reduce transform must be a compute op");
+      if (t->in_kind != read.out_kind) fail(FK_E_KIND_MISMATCH, "reduce transform input kind vs read output");
+      vkind[s] = uint32_t(t->out_kind >= 0 ? t->out_kind : t->in_kind);
+      top[s] = uint32_t(pl.compute.size());
+      pl.compute.push_back(*t);
+    } else {
+      vkind[s] = uint32_t(read.out_kind);
+    }
+  }
+  pl.write.id = FK_OP_PER_THREAD_WRITE;
+  pl.write.opkind = FK_KIND_WRITE;
+  pl.write.in_kind = read.out_kind;
+  pl.write.dest[0] = fk_plane{nullptr, sp.width, sp.height, sp.width, uint32_t(read.out_kind)};
+  DeviceProgram& dp = ensure_program(pl);
+  // the widest lane state any value passes through
+  bool wide = dp.read_wide;
+  int lanes = dp.read_lanes;
+  for (uint32_t k : vkind) add_kind(k, wide, lanes);
+  add_kind(uint32_t(read.out_kind), wide, lanes);
+  const int cls = generic_state_class(wide, lanes);
+  DPlan P = base_plan(sp.width, sp.height, sp.batch, dp.read_flat, reduce_tile_elems());
+  fill_plan_io(P, dp, pl, nullptr);
+  P.reads = dp.d_reads;
+  uint64_t reads_total = 0;
+  for (uint32_t z = 0; z < sp.batch; ++z) {  // sample_raw's touched counts (ops.cpp:312-325)
+    const Sample* smp = read_plane(pl, z);
+    if (!smp) continue;
+    reads_total += uint64_t(sp.width) * sp.height * (smp->resizing() && smp->mode == FK_BILINEAR ? 4 : 1);
+  }
+  if (elements_read) *elements_read = reads_total;
+
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dp.device);
+  const uint64_t tiles = uint64_t(P.tiles) * sp.batch;
+  const uint32_t nblocks = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>((tiles + 255) / 256, uint64_t(sms) * 8)));
+  std::vector<Element> result(specs.size());
+  void* scratch = nullptr;
+  uint64_t* d_out = nullptr;
+  cuda_check(cudaMallocAsync(&scratch, reduce_scratch_bytes(nblocks), st), "cudaMallocAsync");
+  cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_out), 3 * sizeof(uint64_t) * kMaxReduceSpecs, st),
+             "cudaMallocAsync");
+  for (size_t base = 0; base < specs.size(); base += kMaxReduceSpecs) {  // kMaxReduceSpecs specs per traversal
+    RSpecsDev S{};
+    S.n = uint32_t(std::min<size_t>(kMaxReduceSpecs, specs.size() - base));
+    for (uint32_t k = 0; k < S.n; ++k) {
+      const size_t s = base + k;
+      RSpecDev& d = S.s[k];
+      d.op = top[s] == kNoOp ? kNoOp : dp.n_fused + top[s];  // the 1:1 ops follow the fused program
+      d.combine = specs[s].combine;
+      d.lane_kind = lane_kind(vkind[s]);
+      d.lanes = uint32_t(lanes_of(vkind[s]));
+      d.dsum = specs[s].combine == FK_REDUCE_SUM && d.lane_kind != FK_U8;
+      reducer_identity_bits(d.combine, vkind[s], d.ident);
+      if (specs[s].has_identity) element_bits(vkind[s], specs[s].identity, d.user_ident, d.dsum);
+      else if (d.dsum) element_bits(vkind[s], Element{}, d.user_ident, true);  // identity 0 for sums
+      else for (int l = 0; l < 3; ++l) d.user_ident[l] = d.ident[l];
+    }
+    cuda_check(launch_reduce(cls, P, S, scratch, nblocks, d_out, st), "fk_reduce launch");
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    uint64_t h[3 * kMaxReduceSpecs];
+    cuda_check(cudaMemcpyAsync(h, d_out, sizeof(uint64_t) * 3 * S.n, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    for (uint32_t k = 0; k < S.n; ++k) {
+      Element e{};
+      const uint32_t vk = vkind[base + k];
+      for (int l = 0; l < lanes_of(vk); ++l) std::memcpy(e.raw + l * lane_bytes(vk), &h[3 * k + l], lane_bytes(vk));
+      result[base + k] = e;
+    }
+  }
+  cudaFreeAsync(scratch, st);
+  cudaFreeAsync(d_out, st);
+  t_last_kernel = "fk_reduce_partial";
+  return result;
 }
 
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }

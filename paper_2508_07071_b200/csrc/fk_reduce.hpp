@@ -1,0 +1,39 @@
+// fk_reduce.hpp — device-side form of ReduceDPP specs (dpp.hpp:37-41) and the
+// launch entry of fk_reduce.cu.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "fk_devprog.hpp"
+
+namespace fk {
+
+constexpr int kMaxReduceSpecs = 4;     // specs folded per traversal (more: further traversals)
+constexpr uint32_t kNoOp = 0xffffffffu;
+
+struct RSpecDev {
+  uint32_t op;          // index of the transform in the DPlan program table, kNoOp = identity
+  uint32_t combine;     // fk_reducer
+  uint32_t lane_kind;   // FK_U8 / FK_F32 / FK_F64 of the value kind
+  uint32_t lanes;       // 1 or 3
+  uint32_t dsum;        // float Sum: accumulate in double (dpp.cpp:116-127)
+  uint32_t pad;
+  uint64_t ident[3];       // reducer_identity(combine, value kind), lane bits (dpp.cpp:48-73)
+  uint64_t user_ident[3];  // the spec's identity: lane bits, or (dsum) lane values as double bits
+};
+
+struct RSpecsDev {
+  uint32_t n;
+  uint32_t pad;
+  RSpecDev s[kMaxReduceSpecs];
+};
+
+// cls: generic_state_class (32/64-bit lanes x 1/3 lanes); out: 3 lane-bit words per spec (device)
+cudaError_t launch_reduce(int cls, const DPlan& P, const RSpecsDev& S, void* scratch, uint32_t nblocks, uint64_t* out,
+                          cudaStream_t st);
+size_t reduce_scratch_bytes(uint32_t nblocks);
+int reduce_tile_elems();
+
+}  // namespace fk

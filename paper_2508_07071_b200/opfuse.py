@@ -401,6 +401,37 @@ class Library:
     def execute_unfused(self, pipeline, cfg: ExecConfig | None = None) -> ExecReport:
         return self._exec(self._c.fk_execute_unfused, pipeline, cfg)
 
+    def multi_reduce_plane(self, read: IOp, specs, workers: int = 0):
+        """multi_reduce_plane (dpp.hpp:52): specs = [(combine, transform IOp | None,
+        identity Const | None), ...]; returns (list of per-spec lane tuples in the
+        spec's value kind, source elements read). One traversal of the source."""
+        n = len(specs)
+        arr = (_ffi.fk_reduce_spec * max(n, 1))()
+        kinds = []
+        for i, (combine, transform, identity) in enumerate(specs):
+            arr[i].transform = transform._ptr.value if transform is not None else None
+            arr[i].combine = int(combine)
+            if identity is not None:
+                raw = identity.raw()
+                arr[i].has_identity = 1
+                C.memmove(arr[i].identity, raw, len(raw))
+            kinds.append(transform.output_kind if transform is not None and transform.output_kind is not None
+                         else (transform.input_kind if transform is not None else read.output_kind))
+        out = (C.c_uint8 * (24 * max(n, 1)))()
+        reads = C.c_uint64()
+        self._check(self._c.fk_multi_reduce_plane(read._ptr, arr, n, int(workers), out, C.byref(reads)))
+        res = []
+        for i, k in enumerate(kinds):
+            fmt = _STRUCT_FMT[lane_kind(k)]
+            res.append(struct.unpack_from("<" + fmt * LANES[k], bytes(out), 24 * i))
+        return res, reads.value
+
+    def reduce_plane(self, read: IOp, combine: int, transform: IOp | None = None, identity: Const | None = None,
+                     workers: int = 0):
+        """reduce_plane (dpp.hpp:48): one spec."""
+        res, _ = self.multi_reduce_plane(read, [(combine, transform, identity)], workers)
+        return res[0]
+
     def plan_memory_savings(self, pipeline: Pipeline) -> int:
         v = C.c_uint64()
         self._check(self._c.fk_plan_memory_savings(pipeline._ptr, C.byref(v)))

@@ -90,6 +90,28 @@ def _compute(lib, c):
     return _unary(lib, c)
 
 
+def make_read(lib: of.Library, spec: ChainSpec):
+    """The read IOp of `spec` on `lib` (BatchRead when spec.batch) and its source planes."""
+    planes = [lib.plane_from_numpy(a) for a in spec.sources]
+    reads = []
+    for r in spec.reads:
+        src = planes[r.src]
+        op = lib.op_crop(src, r.x0, r.y0, r.w, r.h) if r.w else lib.op_read_per_thread(src)
+        if r.out_w:
+            op = lib.op_resize(op, r.out_w, r.out_h, r.mode)
+        for u in r.post:
+            op = lib.fold_unary_into_read(op, _unary(lib, u))
+        reads.append(op)
+    if spec.batch:
+        dv = of.const_of(reads[0].output_kind, *spec.default) if spec.default is not None else None
+        return lib.op_batch_read(reads, spec.active_read, dv), planes
+    return reads[0], planes
+
+
+def make_compute(lib: of.Library, c):
+    return _compute(lib, c)
+
+
 def instantiate(lib: of.Library, spec: ChainSpec):
     """Build (pipeline, destination planes) for `spec` on `lib`."""
     planes = [lib.plane_from_numpy(a) for a in spec.sources]
