@@ -113,6 +113,7 @@ struct DPlan {
   uint32_t slices;           // CTA slices along z (slots != nullptr)
   uint32_t no_stage;         // 1: column-streaming kernel uses direct tap loads (A/B; FK_SEP_NOSTAGE=1)
   uint32_t dir_rep[4];       // fk_direct: repeat count of chain op k (its constant / reciprocal in aff_c / aff_r [k][0])
+  FastDiv zdiv;              // fk_reduce: n / tiles (plane of a linear tile index)
 };
 constexpr uint32_t kNoPlane = 0xffffffffu;
 

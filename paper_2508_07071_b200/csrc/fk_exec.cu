@@ -1013,6 +1013,7 @@ std::vector<Element> multi_reduce(const Op& read, const std::vector<ReduceSpecHo
   DPlan P = base_plan(sp.width, sp.height, sp.batch, dp.read_flat, reduce_tile_elems());
   fill_plan_io(P, dp, pl, nullptr);
   P.reads = dp.d_reads;
+  P.zdiv = make_fastdiv(P.tiles);
   uint64_t reads_total = 0;
   for (uint32_t z = 0; z < sp.batch; ++z) {  // sample_raw's touched counts (ops.cpp:312-325)
     const Sample* smp = read_plane(pl, z);
@@ -1052,6 +1053,37 @@ std::vector<Element> multi_reduce(const Op& read, const std::vector<ReduceSpecHo
     uint64_t h[3 * kMaxReduceSpecs];
     cuda_check(cudaMemcpyAsync(h, d_out, sizeof(uint64_t) * 3 * S.n, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
     cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+    // a float Max / Min that came out zero: the reference keeps the FIRST zero,
+    // whose sign the order-free fold cannot know -> find the first +0 and -0
+    uint32_t zmask = 0;
+    for (uint32_t k = 0; k < S.n; ++k) {
+      const RSpecDev& d = S.s[k];
+      if (d.combine == FK_REDUCE_SUM || d.lane_kind == FK_U8) continue;
+      for (uint32_t l = 0; l < d.lanes; ++l) {
+        const uint64_t mag = d.lane_kind == FK_F32 ? (h[3 * k + l] & 0x7fffffffu) : (h[3 * k + l] << 1);
+        const bool ident_zero = d.lane_kind == FK_F32 ? (d.user_ident[l] & 0x7fffffffu) == 0 : (d.user_ident[l] << 1) == 0;
+        if (mag == 0 && !ident_zero) zmask |= 1u << (3 * k + l);  // a zero identity comes first and is kept
+      }
+    }
+    if (zmask) {
+      unsigned long long* first = nullptr;
+      cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&first), 6 * kMaxReduceSpecs * sizeof(unsigned long long), st),
+                 "cudaMallocAsync");
+      cuda_check(cudaMemsetAsync(first, 0xff, 6 * kMaxReduceSpecs * sizeof(unsigned long long), st), "cudaMemsetAsync");
+      cuda_check(launch_reduce_zero_sign(cls, P, S, zmask, nblocks, first, st), "fk_reduce_zero_sign launch");
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      unsigned long long hf[6 * kMaxReduceSpecs];
+      cuda_check(cudaMemcpyAsync(hf, first, sizeof hf, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
+      cuda_check(cudaStreamSynchronize(st), "cudaStreamSynchronize");
+      cudaFreeAsync(first, st);
+      for (uint32_t k = 0; k < S.n; ++k)
+        for (uint32_t l = 0; l < 3; ++l) {
+          if (!((zmask >> (3 * k + l)) & 1u)) continue;
+          const bool neg = hf[6 * k + 2 * l + 1] < hf[6 * k + 2 * l];
+          const uint64_t sign = S.s[k].lane_kind == FK_F32 ? 0x80000000ull : 0x8000000000000000ull;
+          h[3 * k + l] = neg ? sign : 0;
+        }
+    }
     for (uint32_t k = 0; k < S.n; ++k) {
       Element e{};
       const uint32_t vk = vkind[base + k];

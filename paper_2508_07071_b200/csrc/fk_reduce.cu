@@ -4,17 +4,17 @@
 // Every thread folds tiles of E consecutive x (grid-stride, coalesced), reading
 // each element once through the same read stage as the fused kernels (crop,
 // resize, batch, default values, folded unaries) and running each spec's
-// transform in registers. Partials then combine through warp shuffles, shared
-// memory and a last single-CTA pass. The fold is made order-independent so the
-// parallel order reproduces the reference's sequential one:
-//   * u8 Sum wraps mod 256 (associative, exact);
-//   * float Sum accumulates in double (the reference does too); the order of
-//     the double additions differs, agreement is within 2^-20 relative
+// transform in registers. Partials combine through warp shuffles, shared
+// memory and a final pass of one CTA per spec. The parallel fold reproduces the
+// reference's sequential one:
+//   * u8 Sum wraps mod 256: accumulated in 32 bits, reduced mod 256 at the end;
+//   * float Sum accumulates in double (as the reference); the order of the
+//     double additions differs, agreement is within 2^-20 relative
 //     (SPEC.md:388), ~2^-40 in practice;
-//   * Max / Min keep "a < b ? b : a": values that compare equal but differ in
-//     bits (+0 / -0) are resolved to the earliest element in (z, y, x) order, so
-//     each partial carries the linear index of its value; NaN is never adopted
-//     (it only survives as a user identity), exactly as in the reference.
+//   * Max / Min keep "a < b ? b : a" (NaN is never adopted). The result is the
+//     FIRST element numerically equal to the extremum; only a zero extremum can
+//     differ in bits (+0 / -0), so when one comes out zero the host runs a
+//     second pass (fk_reduce_zero_sign) that finds the earliest +0 and -0.
 #include <cuda_runtime.h>
 
 #include "fk_launch.hpp"
@@ -28,10 +28,8 @@ namespace {
 constexpr int kRE = 4;            // elements per tile
 constexpr uint32_t kRBlock = 256;  // threads per CTA
 
-struct Acc {          // one spec's partial
-  uint64_t v[3];      // double bits (float Sum) or the value's lane bits
-  uint64_t idx[3];    // Max / Min: 1 + linear index of v[l] (earliest wins ties); 0 = user identity,
-                      // ~0 = default identity (ties with it have identical bits)
+struct Acc {
+  uint64_t v[3];  // double bits (float Sum), 32-bit running u8 sum, or the extremum's lane bits
 };
 
 __device__ __forceinline__ double as_d(uint64_t b) { return __longlong_as_double((long long)b); }
@@ -44,68 +42,138 @@ __device__ __forceinline__ bool lane_less(uint32_t lk, uint64_t a, uint64_t b) {
   return as_d(a) < as_d(b);
 }
 
-__device__ __forceinline__ bool lane_eq(uint32_t lk, uint64_t a, uint64_t b) {  // as numbers: +0 == -0, NaN != NaN
-  if (lk == FK_U8) return (a & 0xffu) == (b & 0xffu);
-  if (lk == FK_F32) return __uint_as_float(uint32_t(a)) == __uint_as_float(uint32_t(b));
-  return as_d(a) == as_d(b);
-}
-
-// fold x (at linear index i) into a, or combine partial x into a
+// a = a (+) x for one spec
 __device__ __forceinline__ void combine(const RSpecDev& s, Acc& a, const Acc& x) {
-  const uint32_t lk = s.lane_kind;
-  if (s.combine == FK_REDUCE_SUM) {
-#pragma unroll
-    for (int l = 0; l < 3; ++l) {
-      if (l >= int(s.lanes)) break;
-      if (s.dsum) a.v[l] = d_bits(as_d(a.v[l]) + as_d(x.v[l]));
-      else a.v[l] = (a.v[l] + x.v[l]) & 0xffu;  // u8_add, scalar.hpp:146-157
-    }
-    return;
-  }
-  // Max: take x where a < x; Min: where x < a; equal values (+0 / -0) -> the
-  // earlier index; unordered (NaN) -> keep a, as the reference's `a < b ? b : a`
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
     if (l >= int(s.lanes)) break;
-    const bool gt = s.combine == FK_REDUCE_MAX ? lane_less(lk, a.v[l], x.v[l]) : lane_less(lk, x.v[l], a.v[l]);
-    if (gt || (lane_eq(lk, a.v[l], x.v[l]) && x.idx[l] < a.idx[l])) {
-      a.v[l] = x.v[l];
-      a.idx[l] = x.idx[l];
+    if (s.combine == FK_REDUCE_SUM) {
+      if (s.dsum) a.v[l] = d_bits(as_d(a.v[l]) + as_d(x.v[l]));
+      else a.v[l] = uint32_t(a.v[l]) + uint32_t(x.v[l]);  // u8_add, mod 256 at the end
+    } else {
+      const bool take = s.combine == FK_REDUCE_MAX ? lane_less(s.lane_kind, a.v[l], x.v[l])
+                                                   : lane_less(s.lane_kind, x.v[l], a.v[l]);
+      if (take) a.v[l] = x.v[l];
     }
   }
 }
 
 __device__ __forceinline__ void identity_acc(const RSpecDev& s, Acc& a) {
 #pragma unroll
-  for (int l = 0; l < 3; ++l) {
-    a.v[l] = s.dsum ? d_bits(0.0) : s.ident[l];
-    a.idx[l] = ~uint64_t(0);
-  }
+  for (int l = 0; l < 3; ++l) a.v[l] = s.dsum ? d_bits(0.0) : (s.combine == FK_REDUCE_SUM ? 0 : s.ident[l]);
 }
 
+// one element's lanes in the accumulator's encoding
 template <class Lane, int L>
-__device__ __forceinline__ void fold_value(const RSpecDev& s, Acc& a, const Lane (&v)[L], uint64_t i) {
+__device__ __forceinline__ Acc as_acc(const RSpecDev& s, const Lane (&v)[L]) {
   Acc x;
 #pragma unroll
   for (int l = 0; l < 3; ++l) {
     const uint64_t b = l < L ? uint64_t(v[l]) : 0;
-    if (s.dsum)
-      x.v[l] = d_bits(s.lane_kind == FK_F32 ? double(__uint_as_float(uint32_t(b))) : as_d(b));
-    else
-      x.v[l] = s.lane_kind == FK_F32 ? (b & 0xffffffffu) : (s.lane_kind == FK_U8 ? (b & 0xffu) : b);
+    if (s.dsum) x.v[l] = d_bits(s.lane_kind == FK_F32 ? double(__uint_as_float(uint32_t(b))) : as_d(b));
+    else x.v[l] = s.lane_kind == FK_F32 ? (b & 0xffffffffu) : (s.lane_kind == FK_U8 ? (b & 0xffu) : b);
   }
-#pragma unroll
-  for (int l = 0; l < 3; ++l) x.idx[l] = i + 1;
-  combine(s, a, x);
+  return x;
 }
 
 __device__ __forceinline__ Acc shfl_down(const Acc& a, int d) {
   Acc r;
 #pragma unroll
   for (int l = 0; l < 3; ++l) r.v[l] = __shfl_down_sync(0xffffffffu, a.v[l], d);
-#pragma unroll
-  for (int l = 0; l < 3; ++l) r.idx[l] = __shfl_down_sync(0xffffffffu, a.idx[l], d);
   return r;
+}
+
+// the tile at linear tile index t: plane z, row y, first column x, element count n
+struct TileAt {
+  uint32_t z, y, x;
+  int n;
+};
+__device__ __forceinline__ TileAt tile_at(const DPlan& P, uint64_t t) {
+  const uint64_t tiles_plane = uint64_t(P.tiles);
+  TileAt a;
+  // plane index: none for one plane, a 32-bit reciprocal division when the
+  // whole space has < 2^32 tiles (P.zdiv), a 64-bit division otherwise
+  a.z = P.batch == 1 ? 0u : (t < (uint64_t(1) << 32) ? dev::fastdiv(uint32_t(t), P.zdiv) : uint32_t(t / tiles_plane));
+  const uint32_t tt = uint32_t(t - uint64_t(a.z) * tiles_plane);
+  a.y = dev::fastdiv(tt, P.tpr);
+  a.x = (tt - a.y * P.tiles_per_row) * kRE;
+  a.n = (P.width - a.x) < uint32_t(kRE) ? int(P.width - a.x) : kRE;
+  return a;
+}
+
+template <class Lane, int L>
+__device__ __forceinline__ void read_tile(const DPlan& P, const TileAt& at, Lane (&v)[kRE][L]) {
+  const DSample s = P.reads[at.z];
+  if constexpr (L == 1) {  // plain u8 / f32 rows, whole aligned tile: one vector load
+    if (s.mode == RD_DIRECT && !(s.flags & SF_DEFAULT) && s.post_len == 0 && at.n == kRE &&
+        (s.kind == FK_F32 || s.kind == FK_U8)) {
+      const uint32_t b = s.kind == FK_F32 ? 4u : 1u;
+      const uint64_t a = s.src + uint64_t(s.y0 + at.y) * s.pitch + uint64_t(s.x0 + at.x) * b;
+      if ((a & (kRE * b - 1)) == 0) {
+        if (s.kind == FK_F32) {
+          const uint4 q = __ldg(reinterpret_cast<const uint4*>(a));
+          v[0][0] = Lane(q.x); v[1][0] = Lane(q.y); v[2][0] = Lane(q.z); v[3][0] = Lane(q.w);
+        } else {
+          const uint32_t q = __ldg(reinterpret_cast<const uint32_t*>(a));
+#pragma unroll
+          for (int e = 0; e < kRE; ++e) v[e][0] = Lane((q >> (8 * e)) & 0xffu);
+        }
+        return;
+      }
+    }
+  }
+  dev::read_raw(P, s, at.x, at.y, at.n, v, nullptr, nullptr);
+  if (!(s.flags & SF_DEFAULT)) dev::run_ops(P, s.post_off, s.post_len, at.z, v);
+}
+
+template <class Lane, int L>
+__device__ __forceinline__ void spec_values(const DPlan& P, const RSpecDev& s, uint32_t z, const Lane (&v)[kRE][L],
+                                            Lane (&w)[kRE][L]) {
+#pragma unroll
+  for (int e = 0; e < kRE; ++e)
+#pragma unroll
+    for (int l = 0; l < L; ++l) w[e][l] = v[e][l];
+  if (s.op != kNoOp) dev::run_ops(P, s.op, 1, z, w);
+}
+
+// Fold a tile's n values into one spec's accumulator, specialised on the
+// combine and the lane kind (the dispatch is per tile and warp-uniform). Every
+// one of the L lanes is folded; lanes beyond the spec's value are never output.
+template <uint32_t CB, uint32_t LK, class Lane, int L>
+__device__ __forceinline__ void fold_tile(Acc& a, const Lane (&w)[kRE][L], int n) {
+#pragma unroll
+  for (int e = 0; e < kRE; ++e) {
+    if (e >= n) break;
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      const uint64_t b = uint64_t(w[e][l]);
+      if constexpr (CB == FK_REDUCE_SUM && LK == FK_U8) {
+        a.v[l] = uint32_t(a.v[l]) + uint32_t(b & 0xffu);
+      } else if constexpr (CB == FK_REDUCE_SUM) {
+        const double x = LK == FK_F32 ? double(__uint_as_float(uint32_t(b))) : as_d(b);
+        a.v[l] = d_bits(as_d(a.v[l]) + x);
+      } else {
+        const uint64_t x = LK == FK_U8 ? (b & 0xffu) : (LK == FK_F32 ? (b & 0xffffffffu) : b);
+        const bool take = CB == FK_REDUCE_MAX ? lane_less(LK, a.v[l], x) : lane_less(LK, x, a.v[l]);
+        if (take) a.v[l] = x;
+      }
+    }
+  }
+}
+
+template <class Lane, int L>
+__device__ __forceinline__ void fold_spec(const RSpecDev& s, Acc& a, const Lane (&w)[kRE][L], int n) {
+  switch (s.combine * 3 + s.lane_kind) {
+    case FK_REDUCE_SUM * 3 + FK_U8: fold_tile<FK_REDUCE_SUM, FK_U8>(a, w, n); break;
+    case FK_REDUCE_SUM * 3 + FK_F32: fold_tile<FK_REDUCE_SUM, FK_F32>(a, w, n); break;
+    case FK_REDUCE_SUM * 3 + FK_F64: fold_tile<FK_REDUCE_SUM, FK_F64>(a, w, n); break;
+    case FK_REDUCE_MAX * 3 + FK_U8: fold_tile<FK_REDUCE_MAX, FK_U8>(a, w, n); break;
+    case FK_REDUCE_MAX * 3 + FK_F32: fold_tile<FK_REDUCE_MAX, FK_F32>(a, w, n); break;
+    case FK_REDUCE_MAX * 3 + FK_F64: fold_tile<FK_REDUCE_MAX, FK_F64>(a, w, n); break;
+    case FK_REDUCE_MIN * 3 + FK_U8: fold_tile<FK_REDUCE_MIN, FK_U8>(a, w, n); break;
+    case FK_REDUCE_MIN * 3 + FK_F32: fold_tile<FK_REDUCE_MIN, FK_F32>(a, w, n); break;
+    default: fold_tile<FK_REDUCE_MIN, FK_F64>(a, w, n); break;
+  }
 }
 
 // CTA partials of every spec: per-thread folds, then warp / CTA combines
@@ -117,31 +185,22 @@ __global__ void __launch_bounds__(kRBlock) fk_reduce_partial(const __grid_consta
 #pragma unroll
   for (int k = 0; k < kMaxReduceSpecs; ++k)
     if (k < int(S.n)) identity_acc(S.s[k], acc[k]);
-  const uint64_t tiles_plane = uint64_t(P.tiles), total = tiles_plane * P.batch;
+  const uint64_t total = uint64_t(P.tiles) * P.batch;
   const uint64_t stride = uint64_t(gridDim.x) * kRBlock;
   for (uint64_t t = uint64_t(blockIdx.x) * kRBlock + threadIdx.x; t < total; t += stride) {
-    const uint32_t z = uint32_t(t / tiles_plane);
-    const uint32_t tt = uint32_t(t - uint64_t(z) * tiles_plane);
-    const uint32_t y = dev::fastdiv(tt, P.tpr);
-    const uint32_t x = (tt - y * P.tiles_per_row) * kRE;
-    const int n = (P.width - x) < uint32_t(kRE) ? int(P.width - x) : kRE;
-    const DSample s = P.reads[z];
+    const TileAt at = tile_at(P, t);
     Lane v[kRE][L];
-    dev::read_raw(P, s, x, y, n, v, nullptr, nullptr);
-    if (!(s.flags & SF_DEFAULT)) dev::run_ops(P, s.post_off, s.post_len, z, v);
-    const uint64_t i0 = (uint64_t(z) * P.height + y) * P.width + x;
+    read_tile<Lane, L>(P, at, v);
 #pragma unroll
     for (int k = 0; k < kMaxReduceSpecs; ++k) {
       if (k >= int(S.n)) break;
-      Lane w[kRE][L];
-#pragma unroll
-      for (int e = 0; e < kRE; ++e)
-#pragma unroll
-        for (int l = 0; l < L; ++l) w[e][l] = v[e][l];
-      if (S.s[k].op != kNoOp) dev::run_ops(P, S.s[k].op, 1, z, w);
-#pragma unroll
-      for (int e = 0; e < kRE; ++e)
-        if (e < n) fold_value<Lane, L>(S.s[k], acc[k], w[e], i0 + e);
+      if (S.s[k].op == kNoOp) {
+        fold_spec<Lane, L>(S.s[k], acc[k], v, at.n);
+      } else {
+        Lane w[kRE][L];
+        spec_values<Lane, L>(P, S.s[k], at.z, v, w);
+        fold_spec<Lane, L>(S.s[k], acc[k], w, at.n);
+      }
     }
   }
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -163,27 +222,72 @@ __global__ void __launch_bounds__(kRBlock) fk_reduce_partial(const __grid_consta
   }
 }
 
-// one thread per spec: CTA partials in order, then identity and finish_accum (dpp.cpp:138-152)
-__global__ void fk_reduce_final(const __grid_constant__ RSpecsDev S, const Acc* partials, uint32_t nparts,
-                                uint64_t* out /* 3 lanes per spec, lane bits in the value kind */) {
-  const int k = int(threadIdx.x);
-  if (k >= int(S.n)) return;
+// one CTA per spec: the CTA partials, then the spec's identity (the left-most
+// operand of the reference's merge, dpp.cpp:232-237) and finish_accum
+// (dpp.cpp:138-152). out: 3 lane words per spec (value kind bits).
+__global__ void __launch_bounds__(kRBlock) fk_reduce_final(const __grid_constant__ RSpecsDev S, const Acc* partials,
+                                                          uint32_t nparts, uint64_t* out) {
+  __shared__ Acc warp_acc[kRBlock / 32];
+  const int k = int(blockIdx.x);
   const RSpecDev& s = S.s[k];
   Acc a;
   identity_acc(s, a);
-  for (uint32_t p = 0; p < nparts; ++p) combine(s, a, partials[uint64_t(p) * kMaxReduceSpecs + k]);
-  if (!s.dsum) {  // the merge starts from the spec's identity (dpp.cpp:232-237): it is the left-most operand
-    Acc r;
-    for (int l = 0; l < 3; ++l) {
-      r.v[l] = s.user_ident[l];
-      r.idx[l] = 0;
-    }
-    combine(s, r, a);
-    for (int l = 0; l < 3; ++l) out[3 * k + l] = r.v[l];
-  } else {
-    for (int l = 0; l < 3; ++l) {
+  for (uint32_t p = threadIdx.x; p < nparts; p += kRBlock) combine(s, a, partials[uint64_t(p) * kMaxReduceSpecs + k]);
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+  for (int d = 16; d > 0; d >>= 1) {
+    const Acc o = shfl_down(a, d);
+    if (lane < uint32_t(d)) combine(s, a, o);
+  }
+  if (lane == 0) warp_acc[warp] = a;
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  a = warp_acc[0];
+  for (uint32_t w = 1; w < kRBlock / 32; ++w) combine(s, a, warp_acc[w]);
+  for (int l = 0; l < 3; ++l) {
+    if (s.dsum) {
       const double total = as_d(s.user_ident[l]) + as_d(a.v[l]);  // identity as double + the sum
       out[3 * k + l] = s.lane_kind == FK_F32 ? uint64_t(__float_as_uint(float(total))) : d_bits(total);
+    } else if (s.combine == FK_REDUCE_SUM) {
+      out[3 * k + l] = (s.user_ident[l] + a.v[l]) & 0xffu;
+    } else {
+      Acc r, m;
+      r.v[0] = r.v[1] = r.v[2] = s.user_ident[l];
+      m.v[0] = m.v[1] = m.v[2] = a.v[l];
+      combine(s, r, m);  // keeps the identity on equality: it comes first
+      out[3 * k + l] = r.v[0];
+    }
+  }
+}
+
+// Second pass for a zero Max / Min: the linear index of the first +0 and of the
+// first -0 of each (spec, lane) flagged in zmask (bit 3 * spec + lane).
+template <class Lane, int L>
+__global__ void __launch_bounds__(kRBlock) fk_reduce_zero_sign(const __grid_constant__ DPlan P,
+                                                             const __grid_constant__ RSpecsDev S, uint32_t zmask,
+                                                             unsigned long long* first) {
+  const uint64_t total = uint64_t(P.tiles) * P.batch;
+  const uint64_t stride = uint64_t(gridDim.x) * kRBlock;
+  for (uint64_t t = uint64_t(blockIdx.x) * kRBlock + threadIdx.x; t < total; t += stride) {
+    const TileAt at = tile_at(P, t);
+    Lane v[kRE][L];
+    read_tile<Lane, L>(P, at, v);
+    const uint64_t i0 = (uint64_t(at.z) * P.height + at.y) * P.width + at.x;
+    for (int k = 0; k < int(S.n); ++k) {
+      if (!((zmask >> (3 * k)) & 7u)) continue;
+      Lane w[kRE][L];
+      spec_values<Lane, L>(P, S.s[k], at.z, v, w);
+      for (int e = 0; e < at.n; ++e) {
+        const Acc x = as_acc<Lane, L>(S.s[k], w[e]);
+        for (int l = 0; l < int(S.s[k].lanes); ++l) {
+          if (!((zmask >> (3 * k + l)) & 1u)) continue;
+          const bool f32 = S.s[k].lane_kind == FK_F32;
+          const uint64_t mag = f32 ? (x.v[l] & 0x7fffffffu) : (x.v[l] & 0x7fffffffffffffffull);
+          if (mag == 0) {
+            const bool neg = f32 ? ((x.v[l] >> 31) & 1u) : ((x.v[l] >> 63) & 1u);
+            atomicMin(first + 6 * k + 2 * l + (neg ? 1 : 0), (unsigned long long)(i0 + e));
+          }
+        }
+      }
     }
   }
 }
@@ -199,7 +303,18 @@ cudaError_t launch_reduce(int cls, const DPlan& P, const RSpecsDev& S, void* scr
     case 2: fk_reduce_partial<uint64_t, 1><<<nblocks, kRBlock, 0, st>>>(P, S, parts); break;
     default: fk_reduce_partial<uint64_t, 3><<<nblocks, kRBlock, 0, st>>>(P, S, parts); break;
   }
-  fk_reduce_final<<<1, 32, 0, st>>>(S, parts, nblocks, out);
+  fk_reduce_final<<<S.n, kRBlock, 0, st>>>(S, parts, nblocks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_zero_sign(int cls, const DPlan& P, const RSpecsDev& S, uint32_t zmask, uint32_t nblocks,
+                                    unsigned long long* first, cudaStream_t st) {
+  switch (cls) {
+    case 0: fk_reduce_zero_sign<uint32_t, 1><<<nblocks, kRBlock, 0, st>>>(P, S, zmask, first); break;
+    case 1: fk_reduce_zero_sign<uint32_t, 3><<<nblocks, kRBlock, 0, st>>>(P, S, zmask, first); break;
+    case 2: fk_reduce_zero_sign<uint64_t, 1><<<nblocks, kRBlock, 0, st>>>(P, S, zmask, first); break;
+    default: fk_reduce_zero_sign<uint64_t, 3><<<nblocks, kRBlock, 0, st>>>(P, S, zmask, first); break;
+  }
   return cudaGetLastError();
 }
 

@@ -33,6 +33,10 @@ struct RSpecsDev {
 // cls: generic_state_class (32/64-bit lanes x 1/3 lanes); out: 3 lane-bit words per spec (device)
 cudaError_t launch_reduce(int cls, const DPlan& P, const RSpecsDev& S, void* scratch, uint32_t nblocks, uint64_t* out,
                           cudaStream_t st);
+// second pass when a float Max / Min came out zero: first +0 / -0 index per
+// (spec, lane) in zmask (bit 3 * spec + lane); first[6 * spec + 2 * lane + neg]
+cudaError_t launch_reduce_zero_sign(int cls, const DPlan& P, const RSpecsDev& S, uint32_t zmask, uint32_t nblocks,
+                                    unsigned long long* first, cudaStream_t st);
 size_t reduce_scratch_bytes(uint32_t nblocks);
 int reduce_tile_elems();
 
