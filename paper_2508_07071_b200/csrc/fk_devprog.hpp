@@ -34,7 +34,8 @@ struct DSample {             // one plane's read (SampleReadParams, ops.hpp:78-9
   uint32_t mode;             // RD_*
   uint32_t post_off, post_len;  // folded unaries: absolute index into the DPlan program table
   uint32_t flags;            // SF_*
-  uint32_t pad;
+  uint32_t tail_bytes;       // bytes readable from the start of the crop's last source row
+                             // (pitch when the view has a row below it, else the row's width)
 };
 
 struct DWrite {              // one plane's write (WriteParams / SplitWriteParams)
@@ -114,6 +115,7 @@ struct DPlan {
   uint32_t no_stage;         // 1: column-streaming kernel uses direct tap loads (A/B; FK_SEP_NOSTAGE=1)
   uint32_t dir_rep[4];       // fk_direct: repeat count of chain op k (its constant / reciprocal in aff_c / aff_r [k][0])
   FastDiv zdiv;              // fk_reduce: n / tiles (plane of a linear tile index)
+  uint32_t ring_span;        // fk_resample_tma: ring bytes per plane slot (16-byte multiple)
 };
 constexpr uint32_t kNoPlane = 0xffffffffu;
 

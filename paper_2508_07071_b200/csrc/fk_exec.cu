@@ -185,6 +185,8 @@ struct DeviceProgram {
   uint32_t* d_slots2 = nullptr;  // column-streaming kernel: planes paired by (mode, rect_h, swap), kNoPlane = none
   uint32_t n_slices2 = 0;        // ... number of pairs
   int stage_ok[2] = {-1, -1};    // staged column walk valid for [single, dual] slices (-1: not yet computed)
+  int tma_ok[2] = {-1, -1};      // bulk-copy producer/consumer walk valid for [single, dual] slices
+  uint32_t tma_span[2] = {0, 0}; // ... its ring bytes per plane slot
   std::vector<void*> extra;      // BatchArith constant tables
   std::vector<DSample> reads;    // host copies
   bool read_flat = false, write_flat = false;
@@ -344,6 +346,11 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
     s.kind = sp->source.kind;
     s.mode = !sp->resizing() ? RD_DIRECT : (sp->mode == FK_NEAREST ? RD_NEAREST : RD_BILINEAR);
     s.flags = lane_aligned(sp->source) ? SF_LANE_ALIGNED : 0;
+    {  // how far a whole-row bulk copy may read in the crop's last row
+      const uint64_t last = uint64_t(sp->y0) + (sp->rect_h ? sp->rect_h : 1) - 1;
+      const uint64_t lim = last + 1 < sp->source.height ? s.pitch : uint64_t(sp->source.width) * bpe(sp->source.kind);
+      s.tail_bytes = uint32_t(std::min<uint64_t>(lim, 0xffffffffu));
+    }
     add_kind(s.kind, dp->read_wide, dp->read_lanes);
     bool post_lane_wise = true, post_swap = false;
     if (!sp->post.empty()) {
@@ -725,6 +732,30 @@ bool sep_stage_ok(const DeviceProgram& dp, uint32_t W, uint32_t T, uint32_t spc)
   return true;
 }
 
+// Can the bulk-copy (TMA) producer/consumer walk run? Bilinear planes with
+// 16-byte aligned rows, one CTA of <= 256 threads per slice, and each plane's
+// 16-byte rounded span inside the source view (DSample::tail_bytes). Returns the
+// ring bytes per plane slot, 0 when not applicable.
+uint32_t sep_tma_span(const DeviceProgram& dp, uint32_t W, uint32_t T, uint32_t spc, uint32_t slices) {
+  if (32 * ((spc * T + 31) / 32 + 1) > 256 || slices > 65535) return 0;
+  uint32_t span = 0;
+  const uint32_t c1 = std::min(2 * T, W);
+  for (const DSample& s : dp.reads) {
+    if (s.flags & SF_DEFAULT) continue;
+    if (s.mode != RD_BILINEAR) return 0;
+    if (((s.src + uint64_t(s.y0) * s.pitch) | s.pitch) & 15) return 0;
+    const uint32_t bpe = uint32_t(lanes_of(s.kind));
+    uint32_t lo, x1, x2, hi;
+    host_taps(s, 0, bpe, lo, x1);
+    host_taps(s, c1 - 1, bpe, x2, hi);
+    lo &= ~15u;
+    const uint32_t bytes = (hi + bpe - lo + 15) & ~15u;
+    if (uint64_t(lo) + bytes > s.tail_bytes) return 0;
+    span = std::max(span, bytes);
+  }
+  return span <= 4096 ? span : 0;
+}
+
 }  // namespace
 
 void check_config(const fk_exec_config* c) {  // executor.cpp:20-25
@@ -811,10 +842,27 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
     S.width = W;
     S.height = H;
     S.tiles_per_cta = uint32_t(band);
-    cuda_check(launch_resample_sep(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)), P.write_mode == WR_SPLIT,
-                                   affine ? dp.aff_sig : kSigLut, S, stage_ok == 1 && !S.no_stage, st),
-               "fk_resample_sep launch");
-    t_last_kernel = "fk_resample_sep";
+    static const bool no_tma = [] {  // the bulk-copy variant is opt-in (slower on C5, see fk_resample_sep.cuh)
+      const char* e = std::getenv("FK_SEP_TMA");
+      return !(e && e[0] == '1');
+    }();
+    int& tma_ok = dp.tma_ok[dual ? 1 : 0];
+    if (tma_ok < 0) {
+      dp.tma_span[dual ? 1 : 0] = sep_tma_span(dp, W, pairs, dual ? 2u : 1u, S.slices);
+      tma_ok = dp.tma_span[dual ? 1 : 0] ? 1 : 0;
+    }
+    if (tma_ok == 1 && !no_tma && !no_stage) {
+      S.ring_span = dp.tma_span[dual ? 1 : 0];
+      cuda_check(launch_resample_tma(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)),
+                                     P.write_mode == WR_SPLIT, affine ? dp.aff_sig : kSigLut, S, st),
+                 "fk_resample_tma launch");
+      t_last_kernel = "fk_resample_tma";
+    } else {
+      cuda_check(launch_resample_sep(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)), P.write_mode == WR_SPLIT,
+                                     affine ? dp.aff_sig : kSigLut, S, stage_ok == 1 && !S.no_stage, st),
+                 "fk_resample_sep launch");
+      t_last_kernel = "fk_resample_sep";
+    }
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     r.path = FK_PATH_COMPILED;
