@@ -265,6 +265,30 @@ __global__ void __launch_bounds__(kBlock, kDirectMinBlocks) fk_direct(const __gr
     const DSample s = P.reads[z];
     const DWrite w = P.writes[z];
     if (!(w.flags & WF_ACTIVE)) continue;
+    if constexpr (kTilesPerIter == 0) {
+      // rolling pipeline over a machine-sized grid: the next tile's loads are in
+      // flight while this tile is computed and stored
+      uint32_t t = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5);
+      if (t >= P.tiles) continue;
+      float cur[kD], nxt[kD];
+      TileAt a = tile_at(P, t);
+      load_tile(P, s, a, lane, cur);
+      for (;;) {
+        const uint32_t tn = t + warps;
+        TileAt b{0, 0};
+        if (tn < P.tiles) {
+          b = tile_at(P, tn);
+          load_tile(P, s, b, lane, nxt);
+        }
+        finish_tile<SIG, TO_U8>(P, w, a, lane, cur, c, r, rep);
+        if (tn >= P.tiles) break;
+        t = tn;
+        a = b;
+#pragma unroll
+        for (int e = 0; e < kD; ++e) cur[e] = nxt[e];
+      }
+      continue;
+    }
     for (uint32_t t = blockIdx.x * (kBlock / 32) + (threadIdx.x >> 5); t < P.tiles; t += kTilesPerIter * warps) {
       float va[kD];
       const TileAt a = tile_at(P, t);
@@ -350,9 +374,10 @@ uint32_t direct_grid_x(K kernel, uint32_t tiles, uint32_t planes) {
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kBlock, 0);
     resident = (sms > 0 ? sms : 148) * (occ > 0 ? occ : 1);
   }
-  const uint64_t per_cta = uint64_t(kTilesPerIter) * (kBlock / 32);  // one loop iteration per warp
+  const uint64_t per_cta = uint64_t(kTilesPerIter ? kTilesPerIter : 1) * (kBlock / 32);  // one iteration per warp
   const uint64_t want = (uint64_t(tiles) + per_cta - 1) / per_cta;
-  const uint64_t cap = (16ull * uint64_t(resident) + planes - 1) / planes;
+  // rolling pipeline (kTilesPerIter == 0): one wave of resident CTAs
+  const uint64_t cap = ((kTilesPerIter ? 16ull : 1ull) * uint64_t(resident) + planes - 1) / planes;
   return uint32_t(want < cap ? (want > 0 ? want : 1) : (cap > 0 ? cap : 1));
 }
 
