@@ -98,20 +98,21 @@ def main():
     rnd = sys.argv[1]
     items = [a for a in sys.argv[2:] if "=" in a]
     launch = sys.argv[sys.argv.index("--launches") + 1] if "--launches" in sys.argv else None
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    path = os.path.join(ROOT, "profiles", f"ncu_summary_{rnd}.json")
+    out_dir = os.environ.get("PROFILES_DIR", os.path.join(ROOT, "profiles"))
+    os.makedirs(out_dir, exist_ok=True)
+    path = os.path.join(out_dir, f"ncu_summary_{rnd}.json")
     summary = json.load(open(path)) if os.path.exists(path) else {}
     for item in items:
         w, rep = item.rsplit("=", 1)
         s = summarise(rep, PX.get(w.split("[")[0]))
         summary[w] = s
-        with open(os.path.join(ROOT, "profiles", f"ncu_{rnd}_{w}.txt"), "w") as f:
+        with open(os.path.join(out_dir, f"ncu_{rnd}_{w}.txt"), "w") as f:
             f.write(json.dumps(s, indent=1) + "\n")
         print(w, s.get("kernel"), s.get("duration_us"), s.get("dram_bytes"))
     with open(path, "w") as f:
         json.dump(summary, f, indent=1)
     if launch:
-        with open(os.path.join(ROOT, "profiles", f"launches_{rnd}.txt"), "w") as f:
+        with open(os.path.join(out_dir, f"launches_{rnd}.txt"), "w") as f:
             f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none ({os.path.basename(launch)})\n")
             f.write(launches(launch) + "\n")
 
