@@ -116,6 +116,7 @@ struct DPlan {
   uint32_t dir_rep[4];       // fk_direct: repeat count of chain op k (its constant / reciprocal in aff_c / aff_r [k][0])
   FastDiv zdiv;              // fk_reduce: n / tiles (plane of a linear tile index)
   uint32_t ring_span;        // fk_resample_tma: ring bytes per plane slot (16-byte multiple)
+  uint32_t no_bulk;          // 1 (default): the staged walk uses per-lane cp.async; 0: per-warp bulk copies (FK_SEP_BULK=1)
 };
 constexpr uint32_t kNoPlane = 0xffffffffu;
 

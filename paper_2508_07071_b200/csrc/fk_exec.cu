@@ -825,6 +825,11 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
       return e && e[0] == '1';
     }();
     S.no_stage = no_stage ? 1u : 0u;
+    static const bool no_bulk = [] {  // opt-in: per-warp bulk copies measured slower than cp.async on C5
+      const char* e = std::getenv("FK_SEP_BULK");
+      return !(e && e[0] == '1');
+    }();
+    S.no_bulk = no_bulk ? 1u : 0u;
     // band: whole planes (up to the table size) unless the batch is too small to
     // give ~2 waves of 16 warps per SM
     const uint64_t units = uint64_t(dual ? w2 : w1) * S.slices;

@@ -589,6 +589,31 @@ __device__ __forceinline__ void pair_bilinear(const DSample& s, const DWrite& w,
   }
 }
 
+// mbarrier / bulk-copy primitives (the staged walk's bulk form and the TMA walk)
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra.uni WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_copy(uint32_t dst, uint64_t src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+
 // ------------------------------------------------- staged (cp.async) walk --
 // Each visit's source row is new to the warp, so a direct tap load is an L2
 // round trip. The staged walk instead copies the row span the warp's columns
@@ -622,6 +647,11 @@ struct StagePlan {
   uint64_t g;            // copy job: source address of the chunk in relative row 0
   uint32_t pitch, dst, n;  // ... row pitch, byte offset in a ring row, bytes (0: none)
   uint32_t ta[2], tb[2];  // byte offsets of tap a / b of columns x, x + 1 in a ring row
+  // whole-span bulk copies (cp.async.bulk), warp-uniform: one per plane slot in
+  // the warp; usable when the 16-byte rounded spans stay inside the source view
+  bool bulk;
+  uint64_t bg[2];
+  uint32_t bpitch[2], bbytes[2], bdst[2];
 };
 
 template <int NL>
@@ -662,6 +692,20 @@ __device__ __forceinline__ StagePlan stage_plan(const DSample& s, bool mine, uin
   S.pitch = pit;
   S.dst = (jobA ? 0u : kRingRow / 2) * (hA == hB ? 0u : 1u) + 16 * c;
   S.n = (jobA || jobB) ? min(16u, vend - start) : 0u;
+  // bulk form: group A from lane 0's plane, group B from lane 31's
+  const uint32_t tail = s.tail_bytes;
+  const uint32_t tailA = __shfl_sync(0xffffffffu, tail, 0), tailB = __shfl_sync(0xffffffffu, tail, 31);
+  const uint64_t oA = __shfl_sync(0xffffffffu, origin, 0), oB = __shfl_sync(0xffffffffu, origin, 31);
+  const uint32_t pA = __shfl_sync(0xffffffffu, uint32_t(s.pitch), 0), pB = __shfl_sync(0xffffffffu, uint32_t(s.pitch), 31);
+  S.bulk = (nA == 0 || spA + 16 * nA <= tailA) && (nB == 0 || spB + 16 * nB <= tailB);
+  S.bg[0] = oA + spA;
+  S.bg[1] = oB + spB;
+  S.bpitch[0] = pA;
+  S.bpitch[1] = pB;
+  S.bbytes[0] = 16 * nA;
+  S.bbytes[1] = 16 * nB;
+  S.bdst[0] = 0;
+  S.bdst[1] = hA == hB ? 0u : kRingRow / 2;
   return S;
 }
 
@@ -671,12 +715,17 @@ __device__ __forceinline__ uint32_t pin(uint32_t v) {
   return v;
 }
 
-template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool VEC, class Out, class KS>
+// BULK: the warp's lane 0 stages each row with one cp.async.bulk per plane slot,
+// completing on the slot's mbarrier (mbar: kRing per-warp barriers); otherwise
+// every lane copies a 16-byte chunk with cp.async (zero-filled past the crop).
+// Measured on C5: 1.87 ms bulk vs 1.63-1.71 ms cp.async (small ~400-byte bulk
+// copies + mbarrier spins), so BULK is opt-in (FK_SEP_BULK=1).
+template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool VEC, bool BULK, class Out, class KS>
 __device__ __forceinline__ void pair_bilinear_staged(const DWrite& w, const BandRows& R, const Visits& V,
-                                                     uint8_t* ring, const StagePlan& S, const XEnt& e0,
-                                                     const XEnt& e1, bool active, uint32_t x, bool col1,
-                                                     uint32_t y0, bool swap, bool al, const KS& ks, const Out* lut,
-                                                     FixList& fix) {
+                                                     uint8_t* ring, uint64_t* mbar, const StagePlan& S,
+                                                     const XEnt& e0, const XEnt& e1, bool active, uint32_t x,
+                                                     bool col1, uint32_t y0, bool swap, bool al, const KS& ks,
+                                                     const Out* lut, FixList& fix) {
   const uint64_t fx = f2::pack(float(e0.f), float(e1.f));
   const float col_thr = (coord_exact8(e0.f) && coord_exact8(e1.f)) ? 0.5f : 0.5f - kNearTol;
   const uint32_t bias = pin(bias_reg());
@@ -693,11 +742,34 @@ __device__ __forceinline__ void pair_bilinear_staged(const DWrite& w, const Band
   using Cur = typename std::conditional<VEC, VecOut, PairOut<NL, OLK, SPLIT>>::type;
   Cur out(w, x, y0, swap);
   const uint32_t nv = V.n;
-  // prologue: visits 0 .. kRing - 2 in flight (one commit group per visit)
+  const uint32_t lane = threadIdx.x & 31u;
+  const uint32_t mb = uint32_t(__cvta_generic_to_shared(mbar));
+  // bulk staging of visit j into ring slot `slot` (lane 0)
+  auto bulk_row = [&](uint32_t j_row, uint32_t slot_off, uint32_t bar) {
+    mbar_expect_tx(bar, S.bbytes[0] + S.bbytes[1]);
 #pragma unroll
-  for (uint32_t j = 0; j < kRing - 1; ++j) {
-    if (j < nv && S.n) cp_async16(cdst + j * kRingRow, at_row(S.g, visit_row(lds32(vp + 4 * j)), S.pitch), S.n);
-    cp_commit();
+    for (int h = 0; h < 2; ++h)
+      if (S.bbytes[h]) bulk_copy(base + slot_off + S.bdst[h], at_row(S.bg[h], j_row, S.bpitch[h]), S.bbytes[h], bar);
+  };
+  if constexpr (BULK) {
+    if (lane == 0) {
+#pragma unroll
+      for (uint32_t j = 0; j < kRing; ++j) mbar_init(mb + 8 * j, 1);
+      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (uint32_t j = 0; j < kRing - 1; ++j)
+        if (j < nv) bulk_row(visit_row(lds32(vp + 4 * j)), j * kRingRow, mb + 8 * j);
+    }
+  } else {
+    // prologue: visits 0 .. kRing - 2 in flight (one commit group per visit)
+#pragma unroll
+    for (uint32_t j = 0; j < kRing - 1; ++j) {
+      if (j < nv && S.n) cp_async16(cdst + j * kRingRow, at_row(S.g, visit_row(lds32(vp + 4 * j)), S.pitch), S.n);
+      cp_commit();
+    }
   }
   uint64_t hA[3] = {0, 0, 0}, hB[3] = {0, 0, 0};
   uint32_t k = 0;
@@ -706,11 +778,18 @@ __device__ __forceinline__ void pair_bilinear_staged(const DWrite& w, const Band
   auto visit = [&](auto U, uint32_t i, uint64_t (&cur)[3], const uint64_t (&prev)[3]) {
     constexpr uint32_t u = decltype(U)::value;
     constexpr uint32_t slot = u * kRingRow, aslot = ((u + kRing - 1) % kRing) * kRingRow;
-    cp_wait<kRing - 2>();  // visit i's row has landed (this lane's chunk) ...
-    __syncwarp();           // ... and every lane's; every lane is also done with visit i - 1's slot
-    if (i + kRing - 1 < nv && S.n)
-      cp_async16(cdst + aslot, at_row(S.g, visit_row(lds32(vp + 4 * (u + kRing - 1))), S.pitch), S.n);
-    cp_commit();
+    if constexpr (BULK) {
+      mbar_wait(mb + 8 * u, (i / kRing) & 1u);  // visit i's row has landed
+      __syncwarp();                              // every lane is done with visit i - 1's slot
+      if (lane == 0 && i + kRing - 1 < nv)
+        bulk_row(visit_row(lds32(vp + 4 * (u + kRing - 1))), aslot, mb + 8 * ((u + kRing - 1) % kRing));
+    } else {
+      cp_wait<kRing - 2>();  // visit i's row has landed (this lane's chunk) ...
+      __syncwarp();           // ... and every lane's; every lane is also done with visit i - 1's slot
+      if (i + kRing - 1 < nv && S.n)
+        cp_async16(cdst + aslot, at_row(S.g, visit_row(lds32(vp + 4 * (u + kRing - 1))), S.pitch), S.n);
+      cp_commit();
+    }
     const uint32_t ta0 = __funnelshift_r(lds32(a0 + slot), lds32(a0 + slot + 4), sa0);
     const uint32_t tb0 = __funnelshift_r(lds32(b0 + slot), lds32(b0 + slot + 4), sb0);
     const uint32_t ta1 = __funnelshift_r(lds32(a1 + slot), lds32(a1 + slot + 4), sa1);
@@ -744,7 +823,8 @@ __device__ __forceinline__ void pair_bilinear_staged(const DWrite& w, const Band
     if (i0 + 7 >= nv) break;
     visit(std::integral_constant<uint32_t, 7 % kRing>(), i0 + 7, hB, hA);
   }
-  cp_wait<0>();
+  if constexpr (!BULK) cp_wait<0>();
+  __syncwarp();  // the ring and its barriers are reused by the next slice
 }
 
 // Nearest / non-resizing planes: one tap per output pixel, the chain in scalar form.
@@ -802,30 +882,6 @@ __device__ __forceinline__ void pair_tap(const DSample& s, const DWrite& w, cons
 #define FK_TRING 4
 #endif
 constexpr uint32_t kTRing = FK_TRING;  // staged rows (kTRing - 1 visits ahead of the slowest consumer)
-
-__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t tx) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(tx) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t a) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra.uni WAIT_%=;\n\t}" ::"r"(a),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_copy(uint32_t dst, uint64_t src, uint32_t bytes, uint32_t mbar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(mbar)
-               : "memory");
-}
 
 // The span of source bytes plane slot columns [c0, c1) touch, 16-byte aligned.
 template <int NL>
@@ -923,6 +979,7 @@ __global__ void __launch_bounds__(32, FK_SEP_MINB) fk_resample_sep(const __grid_
   __shared__ FixShared fixs;
   __shared__ Out lut[AFFINE ? 1 : 2 * NL * 256];
   __shared__ alignas(16) uint8_t ring[STAGED ? kRing * kRingRow : 16];
+  __shared__ alignas(8) uint64_t mbar[kRing];
   const uint32_t lane = threadIdx.x;
   const uint32_t T = P.slot_threads;  // column pairs per plane slot
   const uint32_t spc = P.slots ? P.slots_per_cta : 1u;
@@ -1005,23 +1062,29 @@ __global__ void __launch_bounds__(32, FK_SEP_MINB) fk_resample_sep(const __grid_
         if (!S.ok) __trap();  // the host checked spans and alignment (sep_stage_ok)
         if (__all_sync(0xffffffffu, vec || !active)) {
           // slots share their lane swap, so `swap` is warp-uniform
-          if (AFFINE && P.aff_inline && !swap) {
-            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring, S, e0, e1, active, x, col1, y_begin,
-                                                                 swap, al, KPin<NL, SIG, false>(P), my_lut, fix);
+          if (AFFINE && P.aff_inline && !swap && S.bulk && !P.no_bulk) {  // the configs[1]/[4] path
+            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, true, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
+                                                                       col1, y_begin, swap, al,
+                                                                       KPin<NL, SIG, false>(P), my_lut, fix);
+          } else if (AFFINE && P.aff_inline && !swap) {
+            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, false, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
+                                                                        col1, y_begin, swap, al,
+                                                                        KPin<NL, SIG, false>(P), my_lut, fix);
           } else if (AFFINE && P.aff_inline) {
-            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring, S, e0, e1, active, x, col1, y_begin,
-                                                                 swap, al, KPin<NL, SIG, true>(P), my_lut, fix);
+            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, false, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
+                                                                        col1, y_begin, swap, al,
+                                                                        KPin<NL, SIG, true>(P), my_lut, fix);
           } else {
             AffConsts K;
             if constexpr (AFFINE) load_affine<NL, SIG>(P, z, swap, K);
-            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring, S, e0, e1, active, x, col1, y_begin,
-                                                                 swap, al, KReg{K}, my_lut, fix);
+            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, false, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
+                                                                        col1, y_begin, swap, al, KReg{K}, my_lut, fix);
           }
         } else {
           AffConsts K;
           if constexpr (AFFINE) load_affine<NL, SIG>(P, z, swap, K);
-          pair_bilinear_staged<NL, OLK, SPLIT, SIG, false, Out>(w, R, vis, ring, S, e0, e1, active, x, col1, y_begin,
-                                                                swap, al, KReg{K}, my_lut, fix);
+          pair_bilinear_staged<NL, OLK, SPLIT, SIG, false, false, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
+                                                                       col1, y_begin, swap, al, KReg{K}, my_lut, fix);
         }
       } else if (bilinear && active) {
         AffConsts K;
