@@ -260,16 +260,35 @@ __device__ __forceinline__ float pinf(float v) {
 template <int NL, uint32_t SIG, bool SW>
 struct KPin {
   float cc[3][4], rr[3][4];
-  __device__ __forceinline__ explicit KPin(const DPlan& P) {
+  // staged through shared memory with volatile loads: ptxas may re-read a
+  // kernel parameter inside the loop (LDCU per output row), not a volatile load
+  __device__ __forceinline__ KPin(const DPlan& P, float* scratch) {
+    const uint32_t lane = threadIdx.x & 31u;
+    if (lane == 0) {
+#pragma unroll
+      for (int l = 0; l < 3; ++l)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int m = NL == 3 && SW ? 2 - l : l;
+          scratch[l * 4 + k] = P.aff_c[k][m];
+          scratch[12 + l * 4 + k] = P.aff_r[k][m];
+        }
+    }
+    __syncwarp();
+    const uint32_t sb = uint32_t(__cvta_generic_to_shared(scratch));
 #pragma unroll
     for (int l = 0; l < 3; ++l)
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int m = NL == 3 && SW ? 2 - l : l;
         const bool used = l < NL && k < sig_n(SIG);
-        cc[l][k] = used ? pinf(P.aff_c[k][m]) : 0.f;
-        rr[l][k] = used && sig_fn(SIG, k) == AF_DIV ? pinf(P.aff_r[k][m]) : 0.f;
+        float c = 0.f, r = 0.f;
+        if (used) asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(c) : "r"(sb + 4 * (l * 4 + k)));
+        if (used && sig_fn(SIG, k) == AF_DIV)
+          asm volatile("ld.volatile.shared.f32 %0, [%1];" : "=f"(r) : "r"(sb + 4 * (12 + l * 4 + k)));
+        cc[l][k] = c;
+        rr[l][k] = r;
       }
+    __syncwarp();
   }
   __device__ __forceinline__ float c(int l, int k) const { return cc[l][k]; }
   __device__ __forceinline__ float r(int l, int k) const { return rr[l][k]; }
@@ -980,6 +999,7 @@ __global__ void __launch_bounds__(32, FK_SEP_MINB) fk_resample_sep(const __grid_
   __shared__ Out lut[AFFINE ? 1 : 2 * NL * 256];
   __shared__ alignas(16) uint8_t ring[STAGED ? kRing * kRingRow : 16];
   __shared__ alignas(8) uint64_t mbar[kRing];
+  __shared__ float kscr[24];
   const uint32_t lane = threadIdx.x;
   const uint32_t T = P.slot_threads;  // column pairs per plane slot
   const uint32_t spc = P.slots ? P.slots_per_cta : 1u;
@@ -1065,15 +1085,15 @@ __global__ void __launch_bounds__(32, FK_SEP_MINB) fk_resample_sep(const __grid_
           if (AFFINE && P.aff_inline && !swap && S.bulk && !P.no_bulk) {  // the configs[1]/[4] path
             pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, true, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
                                                                        col1, y_begin, swap, al,
-                                                                       KPin<NL, SIG, false>(P), my_lut, fix);
+                                                                       KPin<NL, SIG, false>(P, kscr), my_lut, fix);
           } else if (AFFINE && P.aff_inline && !swap) {
             pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, false, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
                                                                         col1, y_begin, swap, al,
-                                                                        KPin<NL, SIG, false>(P), my_lut, fix);
+                                                                        KPin<NL, SIG, false>(P, kscr), my_lut, fix);
           } else if (AFFINE && P.aff_inline) {
             pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, false, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
                                                                         col1, y_begin, swap, al,
-                                                                        KPin<NL, SIG, true>(P), my_lut, fix);
+                                                                        KPin<NL, SIG, true>(P, kscr), my_lut, fix);
           } else {
             AffConsts K;
             if constexpr (AFFINE) load_affine<NL, SIG>(P, z, swap, K);
@@ -1133,6 +1153,7 @@ __global__ void __launch_bounds__(256, 3) fk_resample_tma(const __grid_constant_
   __shared__ BandRows R;
   __shared__ Visits vis;
   __shared__ __align__(8) uint64_t bars[2 * kTRing];
+  __shared__ float kscr[24];  // every consumer warp stages the same constants
   __shared__ Out lut[AFFINE ? 1 : 2 * NL * 256];
   const uint32_t spc = P.slots ? P.slots_per_cta : 1u;
   const uint32_t T = P.slot_threads;
@@ -1245,11 +1266,11 @@ __global__ void __launch_bounds__(256, 3) fk_resample_tma(const __grid_constant_
     if (AFFINE && P.aff_inline && !swap)
       pair_bilinear_tma<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring_s, bars_s, slot_bytes, span_lo, region, e0, e1,
                                                         mine, active, x, col1, y_begin, swap, al,
-                                                        KPin<NL, SIG, false>(P), my_lut, fix);
+                                                        KPin<NL, SIG, false>(P, kscr), my_lut, fix);
     else if (AFFINE && P.aff_inline)
       pair_bilinear_tma<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring_s, bars_s, slot_bytes, span_lo, region, e0, e1,
                                                         mine, active, x, col1, y_begin, swap, al,
-                                                        KPin<NL, SIG, true>(P), my_lut, fix);
+                                                        KPin<NL, SIG, true>(P, kscr), my_lut, fix);
     else {
       AffConsts K;
       if constexpr (AFFINE) load_affine<NL, SIG>(P, z, swap, K);
