@@ -270,7 +270,7 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         evs = step_events(lambda i: lib.execute_fused(pipes[i % len(pipes)], cfg), args.steps)
-        kernel = lib._c.fk_cuda_last_kernel().decode()
+        kernel = lib.last_kernel()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()

@@ -11,6 +11,8 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -1079,10 +1081,42 @@ std::vector<Element> multi_reduce(const Op& read, const std::vector<ReduceSpecHo
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dp.device);
   const uint64_t tiles = uint64_t(P.tiles) * sp.batch;
   const uint32_t nblocks = uint32_t(std::max<uint64_t>(1, std::min<uint64_t>((tiles + 255) / 256, uint64_t(sms) * 8)));
+  // one plane of 16-byte aligned single-lane u8 / f32 rows read as they are:
+  // the vector kernel (resident CTAs only, grid-stride)
+  PlainRows R{};
+  bool plain = false;
+  if (std::getenv("FK_DEBUG_REDUCE"))
+    std::fprintf(stderr, "reduce batch=%u cls=%d reads=%zu\n", sp.batch, cls, dp.reads.size());
+  if (sp.batch == 1 && cls == 0 && !dp.reads.empty()) {
+    const DSample& r = dp.reads[0];
+    const uint32_t ve = r.kind == FK_U8 ? 16u : 4u, eb = r.kind == FK_U8 ? 1u : 4u;
+    const uint64_t base = r.src + uint64_t(r.y0) * r.pitch + uint64_t(r.x0) * eb;
+    const uint64_t vpr = (uint64_t(sp.width) + ve - 1) / ve;
+    plain = r.mode == RD_DIRECT && !(r.flags & SF_DEFAULT) && r.post_len == 0 &&
+            (r.kind == FK_U8 || r.kind == FK_F32) && base % 16 == 0 && r.pitch % 16 == 0 &&
+            vpr * sp.height < (uint64_t(1) << 31) && r.pitch * sp.height < (uint64_t(1) << 32) &&
+            std::getenv("FK_REDUCE_GENERIC") == nullptr;
+    if (std::getenv("FK_DEBUG_REDUCE"))
+      std::fprintf(stderr, "reduce plain=%d mode=%u flags=%x post=%u kind=%u base%%16=%llu pitch=%llu vpr=%llu\n",
+                   int(plain), r.mode, r.flags, r.post_len, r.kind, (unsigned long long)(base % 16),
+                   (unsigned long long)r.pitch, (unsigned long long)vpr);
+    if (plain) {
+      R.base = base;
+      R.pitch = r.pitch;
+      R.width = sp.width;
+      R.vpr = uint32_t(vpr);
+      R.vecs = uint32_t(vpr * sp.height);
+      R.kind = r.kind;
+      R.vdiv = make_fastdiv(R.vpr);
+    }
+  }
+  const uint32_t plain_blocks = plain ? std::max<uint32_t>(1, std::min<uint32_t>(reduce_plain_blocks(R.kind, sms),
+                                                                                 (R.vecs + 255) / 256))
+                                      : 0;
   std::vector<Element> result(specs.size());
   void* scratch = nullptr;
   uint64_t* d_out = nullptr;
-  cuda_check(cudaMallocAsync(&scratch, reduce_scratch_bytes(nblocks), st), "cudaMallocAsync");
+  cuda_check(cudaMallocAsync(&scratch, reduce_scratch_bytes(std::max(nblocks, plain_blocks)), st), "cudaMallocAsync");
   cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&d_out), 3 * sizeof(uint64_t) * kMaxReduceSpecs, st),
              "cudaMallocAsync");
   for (size_t base = 0; base < specs.size(); base += kMaxReduceSpecs) {  // kMaxReduceSpecs specs per traversal
@@ -1101,7 +1135,9 @@ std::vector<Element> multi_reduce(const Op& read, const std::vector<ReduceSpecHo
       else if (d.dsum) element_bits(vkind[s], Element{}, d.user_ident, true);  // identity 0 for sums
       else for (int l = 0; l < 3; ++l) d.user_ident[l] = d.ident[l];
     }
-    cuda_check(launch_reduce(cls, P, S, scratch, nblocks, d_out, st), "fk_reduce launch");
+    if (plain) cuda_check(launch_reduce_plain(P, S, R, scratch, plain_blocks, d_out, st), "fk_reduce_plain launch");
+    else cuda_check(launch_reduce(cls, P, S, scratch, nblocks, d_out, st), "fk_reduce launch");
+    t_last_kernel = plain ? (R.kind == FK_U8 ? "fk_reduce_plain<u8>" : "fk_reduce_plain<f32>") : "fk_reduce_partial";
     g_launches.fetch_add(2, std::memory_order_relaxed);
     uint64_t h[3 * kMaxReduceSpecs];
     cuda_check(cudaMemcpyAsync(h, d_out, sizeof(uint64_t) * 3 * S.n, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");
@@ -1146,7 +1182,6 @@ std::vector<Element> multi_reduce(const Op& read, const std::vector<ReduceSpecHo
   }
   cudaFreeAsync(scratch, st);
   cudaFreeAsync(d_out, st);
-  t_last_kernel = "fk_reduce_partial";
   return result;
 }
 

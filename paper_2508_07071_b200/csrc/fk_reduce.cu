@@ -17,6 +17,8 @@
 //     second pass (fk_reduce_zero_sign) that finds the earliest +0 and -0.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "fk_launch.hpp"
 #include "fk_reduce.hpp"
 #include "fk_stages.cuh"
@@ -27,6 +29,13 @@ namespace {
 
 constexpr int kRE = 4;            // elements per tile
 constexpr uint32_t kRBlock = 256;  // threads per CTA
+#ifndef FK_PLAIN_U
+#define FK_PLAIN_U 2
+#endif
+#ifndef FK_PLAIN_MINB
+#define FK_PLAIN_MINB 4
+#endif
+constexpr int kPlainU = FK_PLAIN_U;  // vectors in flight per thread (plain rows)
 
 struct Acc {
   uint64_t v[3];  // double bits (float Sum), 32-bit running u8 sum, or the extremum's lane bits
@@ -139,10 +148,10 @@ __device__ __forceinline__ void spec_values(const DPlan& P, const RSpecDev& s, u
 // Fold a tile's n values into one spec's accumulator, specialised on the
 // combine and the lane kind (the dispatch is per tile and warp-uniform). Every
 // one of the L lanes is folded; lanes beyond the spec's value are never output.
-template <uint32_t CB, uint32_t LK, class Lane, int L>
-__device__ __forceinline__ void fold_tile(Acc& a, const Lane (&w)[kRE][L], int n) {
+template <uint32_t CB, uint32_t LK, class Lane, int E, int L>
+__device__ __forceinline__ void fold_tile(Acc& a, const Lane (&w)[E][L], int n) {
 #pragma unroll
-  for (int e = 0; e < kRE; ++e) {
+  for (int e = 0; e < E; ++e) {
     if (e >= n) break;
 #pragma unroll
     for (int l = 0; l < L; ++l) {
@@ -161,8 +170,8 @@ __device__ __forceinline__ void fold_tile(Acc& a, const Lane (&w)[kRE][L], int n
   }
 }
 
-template <class Lane, int L>
-__device__ __forceinline__ void fold_spec(const RSpecDev& s, Acc& a, const Lane (&w)[kRE][L], int n) {
+template <class Lane, int E, int L>
+__device__ __forceinline__ void fold_spec(const RSpecDev& s, Acc& a, const Lane (&w)[E][L], int n) {
   switch (s.combine * 3 + s.lane_kind) {
     case FK_REDUCE_SUM * 3 + FK_U8: fold_tile<FK_REDUCE_SUM, FK_U8>(a, w, n); break;
     case FK_REDUCE_SUM * 3 + FK_F32: fold_tile<FK_REDUCE_SUM, FK_F32>(a, w, n); break;
@@ -195,12 +204,230 @@ __global__ void __launch_bounds__(kRBlock) fk_reduce_partial(const __grid_consta
     for (int k = 0; k < kMaxReduceSpecs; ++k) {
       if (k >= int(S.n)) break;
       if (S.s[k].op == kNoOp) {
-        fold_spec<Lane, L>(S.s[k], acc[k], v, at.n);
+        fold_spec<Lane, kRE, L>(S.s[k], acc[k], v, at.n);
       } else {
         Lane w[kRE][L];
         spec_values<Lane, L>(P, S.s[k], at.z, v, w);
-        fold_spec<Lane, L>(S.s[k], acc[k], w, at.n);
+        fold_spec<Lane, kRE, L>(S.s[k], acc[k], w, at.n);
       }
+    }
+  }
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kMaxReduceSpecs; ++k) {
+    if (k >= int(S.n)) break;
+    for (int d = 16; d > 0; d >>= 1) {
+      const Acc o = shfl_down(acc[k], d);
+      if (lane < uint32_t(d)) combine(S.s[k], acc[k], o);
+    }
+    if (lane == 0) warp_acc[warp][k] = acc[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < uint32_t(S.n)) {
+    const int k = int(threadIdx.x);
+    Acc a = warp_acc[0][k];
+    for (uint32_t w = 1; w < kRBlock / 32; ++w) combine(S.s[k], a, warp_acc[w][k]);
+    partials[uint64_t(blockIdx.x) * kMaxReduceSpecs + k] = a;
+  }
+}
+
+// Plain single-lane rows (one plane, direct read, no default values or folded
+// unaries, 16-byte aligned rows): each thread folds 16-byte vectors (16 u8 or
+// 4 f32), two in flight per iteration, with the read stage's bookkeeping
+// reduced to one reciprocal division per vector.
+// A thread's walk over the vectors v, v + stride, ...: a 32-bit byte offset
+// from the plane's first element (the host keeps the plane under 4 GiB) that
+// advances by the stride's (rows, vectors) with one carry, no division.
+struct PlainCursor {
+  uint32_t off;  // byte offset of the vector
+  uint32_t xv;   // vector index in its row
+};
+
+__device__ __forceinline__ PlainCursor plain_start(const PlainRows& R, uint32_t v) {
+  const uint32_t y = dev::fastdiv(v, R.vdiv);
+  const uint32_t xv = v - y * R.vpr;
+  return PlainCursor{y * uint32_t(R.pitch) + xv * 16u, xv};
+}
+
+__device__ __forceinline__ void plain_advance(const PlainRows& R, PlainCursor& c, uint32_t sx, uint32_t dstep,
+                                              uint32_t wrap) {
+  c.off += dstep;
+  c.xv += sx;
+  if (c.xv >= R.vpr) {
+    c.xv -= R.vpr;
+    c.off += wrap;
+  }
+}
+
+// the row's last, partial vector (its bytes past the row are never touched)
+template <uint32_t KIND>
+__device__ __noinline__ uint4 plain_partial(uint64_t a, uint32_t n) {
+  uint32_t w[4] = {0, 0, 0, 0};
+  for (uint32_t e = 0; e < n; ++e) {
+    const uint32_t b = KIND == FK_U8 ? uint32_t(*reinterpret_cast<const uint8_t*>(a + e))
+                                     : *reinterpret_cast<const uint32_t*>(a + 4 * e);
+    if (KIND == FK_U8) w[e >> 2] |= b << (8 * (e & 3)); else w[e] = b;
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+template <uint32_t KIND>
+__device__ __forceinline__ int plain_load(const PlainRows& R, const PlainCursor& c, uint4& q) {
+  constexpr uint32_t VE = KIND == FK_U8 ? 16u : 4u;
+  const uint32_t left = R.width - c.xv * VE;
+  const uint64_t a = R.base + c.off;
+  if (left >= VE) {
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "l"(a));
+    return int(VE);
+  }
+  q = plain_partial<KIND>(a, left);
+  return int(left);
+}
+
+// The general fold of one spec over one vector (a transform, or a partial
+// vector at a row's end): out of line, accumulator in and out by value, so the
+// hot loop's code stays small and its accumulators stay in registers.
+template <uint32_t KIND>
+__device__ __noinline__ uint64_t fold_vector_general(const DPlan& P, const RSpecDev& s, uint64_t a0, uint4 q, int n) {
+  constexpr int VE = KIND == FK_U8 ? 16 : 4;
+  Acc a;
+  a.v[0] = a0;
+  a.v[1] = a.v[2] = 0;
+  uint32_t w[VE][1];
+  const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+  for (int e = 0; e < VE; ++e) w[e][0] = KIND == FK_U8 ? (qw[e >> 2] >> (8 * (e & 3))) & 0xffu : qw[e];
+  if (s.op != kNoOp) dev::run_ops(P, s.op, 1, 0, w);
+  fold_spec<uint32_t, VE, 1>(s, a, w, n);
+  return a.v[0];
+}
+
+// A whole vector, no transform.
+//   f32 Sum: a pairwise tree in double (the order of the double additions is
+//     free within the 2^-20 agreement);
+//   f32 Max / Min: fmaxf / fminf trees, which keep "a < b ? b : a"'s value (NaN
+//     never adopted; only the sign of a zero result can differ, and the
+//     zero-sign pass settles that);
+//   u8 Sum: dp4a into the running 32-bit sum (only ever read mod 256);
+//   u8 Max / Min: the bytes as two 16-bit lanes per word (even / odd bytes),
+//     folded with VIMNMX.U16x2 into a packed accumulator pk that is reduced
+//     horizontally once, after the walk.
+struct U8Split {
+  uint32_t e[4], o[4];
+};
+__device__ __forceinline__ U8Split u8_split(const uint4& q) {
+  const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+  U8Split r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    r.e[i] = w[i] & 0x00ff00ffu;
+    r.o[i] = (w[i] >> 8) & 0x00ff00ffu;
+  }
+  return r;
+}
+__device__ __forceinline__ uint32_t mm2(uint32_t a, uint32_t b, bool mx) { return mx ? __vmaxu2(a, b) : __vminu2(a, b); }
+
+template <uint32_t KIND>
+__device__ __forceinline__ void fold_vector_fast(const RSpecDev& s, uint64_t& a0, uint32_t& pk, const uint4& q,
+                                                 const U8Split& sp) {
+  if constexpr (KIND == FK_U8) {
+    if (s.combine == FK_REDUCE_SUM) {
+      uint32_t t = uint32_t(a0);
+      t = __dp4a(q.x, 0x01010101u, t);
+      t = __dp4a(q.y, 0x01010101u, t);
+      t = __dp4a(q.z, 0x01010101u, t);
+      t = __dp4a(q.w, 0x01010101u, t);
+      a0 = t;
+    } else {
+      const bool mx = s.combine == FK_REDUCE_MAX;
+      const uint32_t m = mm2(mm2(mm2(sp.e[0], sp.o[0], mx), mm2(sp.e[1], sp.o[1], mx), mx),
+                             mm2(mm2(sp.e[2], sp.o[2], mx), mm2(sp.e[3], sp.o[3], mx), mx), mx);
+      pk = mm2(pk, m, mx);
+    }
+  } else {
+    const float x0 = __uint_as_float(q.x), x1 = __uint_as_float(q.y), x2 = __uint_as_float(q.z),
+                x3 = __uint_as_float(q.w);
+    if (s.combine == FK_REDUCE_SUM) {
+      const double t = (double(x0) + double(x1)) + (double(x2) + double(x3));
+      a0 = d_bits(as_d(a0) + t);
+    } else if (s.combine == FK_REDUCE_MAX) {
+      a0 = __float_as_uint(fmaxf(__uint_as_float(uint32_t(a0)), fmaxf(fmaxf(x0, x1), fmaxf(x2, x3))));
+    } else {
+      a0 = __float_as_uint(fminf(__uint_as_float(uint32_t(a0)), fminf(fminf(x0, x1), fminf(x2, x3))));
+    }
+  }
+}
+
+template <uint32_t KIND>
+__device__ __forceinline__ void plain_fold(const DPlan& P, const RSpecsDev& S, uint64_t (&acc)[kMaxReduceSpecs],
+                                           uint32_t (&pk)[kMaxReduceSpecs], const uint4& q, int n) {
+  constexpr int VE = KIND == FK_U8 ? 16 : 4;
+  const U8Split sp = KIND == FK_U8 ? u8_split(q) : U8Split{};
+#pragma unroll
+  for (int k = 0; k < kMaxReduceSpecs; ++k) {
+    if (k >= int(S.n)) break;
+    const RSpecDev& s = S.s[k];
+    if (s.op == kNoOp && n == VE) fold_vector_fast<KIND>(s, acc[k], pk[k], q, sp);
+    else acc[k] = fold_vector_general<KIND>(P, s, acc[k], q, n);
+  }
+}
+
+template <uint32_t KIND>
+__global__ void __launch_bounds__(kRBlock, FK_PLAIN_MINB) fk_reduce_plain(const __grid_constant__ DPlan P,
+                                                                         const __grid_constant__ RSpecsDev S,
+                                                                         const __grid_constant__ PlainRows R,
+                                                                         Acc* partials) {
+  __shared__ Acc warp_acc[kRBlock / 32][kMaxReduceSpecs];
+  uint64_t a1[kMaxReduceSpecs];  // single-lane accumulators
+  uint32_t pk[kMaxReduceSpecs];  // u8 Max / Min: packed 16x2 accumulators
+#pragma unroll
+  for (int k = 0; k < kMaxReduceSpecs; ++k) {
+    Acc i;
+    identity_acc(S.s[k], i);
+    a1[k] = i.v[0];
+    pk[k] = uint32_t(i.v[0] & 0xffu) * 0x00010001u;
+  }
+  const uint32_t total = R.vecs;
+  const uint32_t stride = gridDim.x * kRBlock;
+  uint32_t v = blockIdx.x * kRBlock + threadIdx.x;
+  if (v < total) {
+    const uint32_t sy = dev::fastdiv(stride, R.vdiv), sx = stride - sy * R.vpr;
+    const uint32_t dstep = sy * uint32_t(R.pitch) + sx * 16u;
+    const uint32_t wrap = uint32_t(R.pitch) - R.vpr * 16u;
+    PlainCursor c = plain_start(R, v);
+    for (; v + (kPlainU - 1) * stride < total; v += kPlainU * stride) {  // kPlainU loads in flight
+      uint4 q[kPlainU];
+      int n[kPlainU];
+#pragma unroll
+      for (int u = 0; u < kPlainU; ++u) {
+        n[u] = plain_load<KIND>(R, c, q[u]);
+        plain_advance(R, c, sx, dstep, wrap);
+      }
+#ifdef FK_PLAIN_PROBE  // memory-only probe: no fold
+#pragma unroll
+      for (int u = 0; u < kPlainU; ++u) a1[0] ^= q[u].x ^ q[u].y ^ q[u].z ^ q[u].w ^ n[u];
+#else
+#pragma unroll
+      for (int u = 0; u < kPlainU; ++u) plain_fold<KIND>(P, S, a1, pk, q[u], n[u]);
+#endif
+    }
+    for (; v < total; v += stride) {
+      uint4 q;
+      const int n = plain_load<KIND>(R, c, q);
+      plain_advance(R, c, sx, dstep, wrap);
+      plain_fold<KIND>(P, S, a1, pk, q, n);
+    }
+  }
+  Acc acc[kMaxReduceSpecs];
+#pragma unroll
+  for (int k = 0; k < kMaxReduceSpecs; ++k) {
+    acc[k].v[0] = a1[k];
+    acc[k].v[1] = acc[k].v[2] = 0;
+    if (KIND == FK_U8 && S.s[k].combine != FK_REDUCE_SUM) {  // the packed lanes' extremum joins the scalar one
+      const bool mx = S.s[k].combine == FK_REDUCE_MAX;
+      const uint32_t m = mm2(pk[k], pk[k] >> 16, mx) & 0xffu;
+      if (mx ? uint32_t(a1[k]) < m : m < uint32_t(a1[k])) acc[k].v[0] = m;
     }
   }
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -232,7 +459,15 @@ __global__ void __launch_bounds__(kRBlock) fk_reduce_final(const __grid_constant
   const RSpecDev& s = S.s[k];
   Acc a;
   identity_acc(s, a);
-  for (uint32_t p = threadIdx.x; p < nparts; p += kRBlock) combine(s, a, partials[uint64_t(p) * kMaxReduceSpecs + k]);
+  uint32_t p = threadIdx.x;
+  for (; p + 3 * kRBlock < nparts; p += 4 * kRBlock) {  // four partials in flight
+    Acc x[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) x[u] = partials[uint64_t(p + u * kRBlock) * kMaxReduceSpecs + k];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) combine(s, a, x[u]);
+  }
+  for (; p < nparts; p += kRBlock) combine(s, a, partials[uint64_t(p) * kMaxReduceSpecs + k]);
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
   for (int d = 16; d > 0; d >>= 1) {
     const Acc o = shfl_down(a, d);
@@ -316,6 +551,22 @@ cudaError_t launch_reduce_zero_sign(int cls, const DPlan& P, const RSpecsDev& S,
     default: fk_reduce_zero_sign<uint64_t, 3><<<nblocks, kRBlock, 0, st>>>(P, S, zmask, first); break;
   }
   return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_plain(const DPlan& P, const RSpecsDev& S, const PlainRows& R, void* scratch,
+                                uint32_t nblocks, uint64_t* out, cudaStream_t st) {
+  Acc* parts = static_cast<Acc*>(scratch);
+  if (R.kind == FK_U8) fk_reduce_plain<FK_U8><<<nblocks, kRBlock, 0, st>>>(P, S, R, parts);
+  else fk_reduce_plain<FK_F32><<<nblocks, kRBlock, 0, st>>>(P, S, R, parts);
+  fk_reduce_final<<<S.n, kRBlock, 0, st>>>(S, parts, nblocks, out);
+  return cudaGetLastError();
+}
+
+uint32_t reduce_plain_blocks(uint32_t kind, int sms) {
+  int per_sm = 0;
+  if (kind == FK_U8) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk_reduce_plain<FK_U8>, kRBlock, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk_reduce_plain<FK_F32>, kRBlock, 0);
+  return uint32_t(std::max(1, per_sm)) * uint32_t(sms);
 }
 
 size_t reduce_scratch_bytes(uint32_t nblocks) { return size_t(nblocks) * kMaxReduceSpecs * sizeof(Acc); }

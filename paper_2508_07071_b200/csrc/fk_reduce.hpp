@@ -30,6 +30,18 @@ struct RSpecsDev {
   RSpecDev s[kMaxReduceSpecs];
 };
 
+// a plain read: one plane of single-lane u8 / f32 rows, 16-byte aligned, no
+// default values or folded unaries, walked as 16-byte vectors
+struct PlainRows {
+  uint64_t base;   // address of element (0, 0)
+  uint64_t pitch;  // bytes per row (multiple of 16)
+  uint32_t width;  // elements per row
+  uint32_t vpr;    // vectors per row
+  uint32_t vecs;   // rows * vpr (< 2^32)
+  uint32_t kind;   // FK_U8 / FK_F32
+  FastDiv vdiv;    // / vpr
+};
+
 // cls: generic_state_class (32/64-bit lanes x 1/3 lanes); out: 3 lane-bit words per spec (device)
 cudaError_t launch_reduce(int cls, const DPlan& P, const RSpecsDev& S, void* scratch, uint32_t nblocks, uint64_t* out,
                           cudaStream_t st);
@@ -37,6 +49,9 @@ cudaError_t launch_reduce(int cls, const DPlan& P, const RSpecsDev& S, void* scr
 // (spec, lane) in zmask (bit 3 * spec + lane); first[6 * spec + 2 * lane + neg]
 cudaError_t launch_reduce_zero_sign(int cls, const DPlan& P, const RSpecsDev& S, uint32_t zmask, uint32_t nblocks,
                                     unsigned long long* first, cudaStream_t st);
+cudaError_t launch_reduce_plain(const DPlan& P, const RSpecsDev& S, const PlainRows& R, void* scratch,
+                                uint32_t nblocks, uint64_t* out, cudaStream_t st);
+uint32_t reduce_plain_blocks(uint32_t kind, int sms);  // resident CTAs on the device
 size_t reduce_scratch_bytes(uint32_t nblocks);
 int reduce_tile_elems();
 

@@ -401,6 +401,10 @@ class Library:
     def execute_unfused(self, pipeline, cfg: ExecConfig | None = None) -> ExecReport:
         return self._exec(self._c.fk_execute_unfused, pipeline, cfg)
 
+    def last_kernel(self) -> str:
+        """Kernel family of this thread's last execute / reduce (CUDA backend only)."""
+        return self._c.fk_cuda_last_kernel().decode()
+
     def multi_reduce_plane(self, read: IOp, specs, workers: int = 0):
         """multi_reduce_plane (dpp.hpp:52): specs = [(combine, transform IOp | None,
         identity Const | None), ...]; returns (list of per-spec lane tuples in the

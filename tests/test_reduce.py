@@ -179,3 +179,34 @@ def test_cuda_large_u8x3_and_many_specs(oracle):
     kinds = [U8X3, U8X3, U8X3, F64X3, U8X3, U8X3]
     for x, y, (c, _, _), k in zip(res[0][0], res[1][0], specs_of(oracle), kinds):
         close(x, y, c, k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dt,kind", [(np.uint8, U8), (np.float32, F32)])
+def test_cuda_plain_rows(oracle, dt, kind):
+    """One plane of 16-byte aligned single-lane rows: the vector kernel
+    (fk_reduce_plain). Crops whose width is not a multiple of the vector leave a
+    partial last vector per row; transforms run per spec; -0 / NaN included."""
+    cuda = Library("cuda")
+    rng = np.random.default_rng(21)
+    big = (rng.integers(0, 256, (517, 1024), dtype=np.uint8) if dt == np.uint8
+           else rng.standard_normal((517, 1024)).astype(np.float32))
+    if dt == np.float32:
+        big[rng.random(big.shape) < 0.001] = np.nan
+    crops = [(0, 0, 1024, 517), (16, 3, 37, 200), (16, 0, 1000, 1), (0, 1, 5, 516), (64, 5, 960, 511), (3, 2, 50, 50)]
+    for x0, y0, w, h in crops:
+        specs_of = lambda lib: [(REDUCE_SUM, None, None), (REDUCE_MAX, None, None), (REDUCE_MIN, None, None),  # noqa
+                                (REDUCE_SUM, lib.make_arith(8, of.const_of(kind, 3)), None),
+                                (REDUCE_MAX, lib.op_cast(kind, F32 if kind == U8 else U8), of.const_of(
+                                    F32 if kind == U8 else U8, 7))]
+        res = []
+        for lib in (cuda, oracle):
+            p = lib.plane_from_numpy(big)
+            r = lib.op_crop(p, x0, y0, w, h) if (w, h) != big.shape[::-1] else lib.op_read_per_thread(p)
+            res.append(lib.multi_reduce_plane(r, specs_of(lib)))
+        assert res[0][1] == res[1][1] == w * h
+        if (x0, y0, w, h) == crops[0] or x0 % 16 == 0:
+            assert cuda.last_kernel().startswith("fk_reduce_plain"), cuda.last_kernel()
+        kinds = [kind, kind, kind, kind, F32 if kind == U8 else U8]
+        for x, y, (c, _, _), k in zip(res[0][0], res[1][0], specs_of(oracle), kinds):
+            close(x, y, c, k)

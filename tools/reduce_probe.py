@@ -6,10 +6,11 @@ from paper_2508_07071_b200.opfuse import Library
 from paper_2508_07071_b200._ffi import REDUCE_SUM, REDUCE_MAX, REDUCE_MIN
 lib = Library("cuda")
 rng = np.random.default_rng(0)
-for shape, dt in (((2160, 3840), np.float32), ((8192, 8192), np.float32), ((1080, 1920, 3), np.uint8)):
+for shape, dt in (((2160, 3840), np.float32), ((8192, 8192), np.float32), ((1080, 1920, 3), np.uint8), ((8192, 8192), np.uint8)):
     a = (rng.random(shape, dtype=np.float32) if dt == np.float32 else rng.integers(0, 256, shape, dtype=np.uint8))
     r = lib.op_read_per_thread(lib.plane_from_numpy(a))
-    specs = [(REDUCE_SUM, None, None), (REDUCE_MAX, None, None), (REDUCE_MIN, None, None)]
+    which = os.environ.get("SPECS", "sum,max,min").split(",")
+    specs = [({"sum": REDUCE_SUM, "max": REDUCE_MAX, "min": REDUCE_MIN}[w], None, None) for w in which]
     for _ in range(3):
         res, n = lib.multi_reduce_plane(r, specs)
     t = time.time()
