@@ -1087,13 +1087,13 @@ std::vector<Element> multi_reduce(const Op& read, const std::vector<ReduceSpecHo
   bool plain = false;
   if (std::getenv("FK_DEBUG_REDUCE"))
     std::fprintf(stderr, "reduce batch=%u cls=%d reads=%zu\n", sp.batch, cls, dp.reads.size());
-  if (sp.batch == 1 && cls == 0 && !dp.reads.empty()) {
+  if (sp.batch == 1 && !dp.reads.empty() && (cls == 0 || (cls == 1 && dp.reads[0].kind == FK_U8X3))) {
     const DSample& r = dp.reads[0];
-    const uint32_t ve = r.kind == FK_U8 ? 16u : 4u, eb = r.kind == FK_U8 ? 1u : 4u;
+    const uint32_t ve = r.kind == FK_F32 ? 4u : 16u, eb = r.kind == FK_F32 ? 4u : (r.kind == FK_U8X3 ? 3u : 1u);
     const uint64_t base = r.src + uint64_t(r.y0) * r.pitch + uint64_t(r.x0) * eb;
     const uint64_t vpr = (uint64_t(sp.width) + ve - 1) / ve;
     plain = r.mode == RD_DIRECT && !(r.flags & SF_DEFAULT) && r.post_len == 0 &&
-            (r.kind == FK_U8 || r.kind == FK_F32) && base % 16 == 0 && r.pitch % 16 == 0 &&
+            (r.kind == FK_U8 || r.kind == FK_F32 || r.kind == FK_U8X3) && base % 16 == 0 && r.pitch % 16 == 0 &&
             vpr * sp.height < (uint64_t(1) << 31) && r.pitch * sp.height < (uint64_t(1) << 32) &&
             std::getenv("FK_REDUCE_GENERIC") == nullptr;
     if (std::getenv("FK_DEBUG_REDUCE"))
@@ -1107,6 +1107,7 @@ std::vector<Element> multi_reduce(const Op& read, const std::vector<ReduceSpecHo
       R.vpr = uint32_t(vpr);
       R.vecs = uint32_t(vpr * sp.height);
       R.kind = r.kind;
+      R.vb = ve * eb;
       R.vdiv = make_fastdiv(R.vpr);
     }
   }
@@ -1137,7 +1138,9 @@ std::vector<Element> multi_reduce(const Op& read, const std::vector<ReduceSpecHo
     }
     if (plain) cuda_check(launch_reduce_plain(P, S, R, scratch, plain_blocks, d_out, st), "fk_reduce_plain launch");
     else cuda_check(launch_reduce(cls, P, S, scratch, nblocks, d_out, st), "fk_reduce launch");
-    t_last_kernel = plain ? (R.kind == FK_U8 ? "fk_reduce_plain<u8>" : "fk_reduce_plain<f32>") : "fk_reduce_partial";
+    t_last_kernel = !plain ? "fk_reduce_partial"
+                           : (R.kind == FK_U8 ? "fk_reduce_plain<u8>"
+                                              : (R.kind == FK_U8X3 ? "fk_reduce_plain<u8x3>" : "fk_reduce_plain<f32>"));
     g_launches.fetch_add(2, std::memory_order_relaxed);
     uint64_t h[3 * kMaxReduceSpecs];
     cuda_check(cudaMemcpyAsync(h, d_out, sizeof(uint64_t) * 3 * S.n, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");

@@ -246,7 +246,7 @@ struct PlainCursor {
 __device__ __forceinline__ PlainCursor plain_start(const PlainRows& R, uint32_t v) {
   const uint32_t y = dev::fastdiv(v, R.vdiv);
   const uint32_t xv = v - y * R.vpr;
-  return PlainCursor{y * uint32_t(R.pitch) + xv * 16u, xv};
+  return PlainCursor{y * uint32_t(R.pitch) + xv * R.vb, xv};
 }
 
 __device__ __forceinline__ void plain_advance(const PlainRows& R, PlainCursor& c, uint32_t sx, uint32_t dstep,
@@ -393,8 +393,8 @@ __global__ void __launch_bounds__(kRBlock, FK_PLAIN_MINB) fk_reduce_plain(const 
   uint32_t v = blockIdx.x * kRBlock + threadIdx.x;
   if (v < total) {
     const uint32_t sy = dev::fastdiv(stride, R.vdiv), sx = stride - sy * R.vpr;
-    const uint32_t dstep = sy * uint32_t(R.pitch) + sx * 16u;
-    const uint32_t wrap = uint32_t(R.pitch) - R.vpr * 16u;
+    const uint32_t dstep = sy * uint32_t(R.pitch) + sx * R.vb;
+    const uint32_t wrap = uint32_t(R.pitch) - R.vpr * R.vb;
     PlainCursor c = plain_start(R, v);
     for (; v + (kPlainU - 1) * stride < total; v += kPlainU * stride) {  // kPlainU loads in flight
       uint4 q[kPlainU];
@@ -428,6 +428,126 @@ __global__ void __launch_bounds__(kRBlock, FK_PLAIN_MINB) fk_reduce_plain(const 
       const bool mx = S.s[k].combine == FK_REDUCE_MAX;
       const uint32_t m = mm2(pk[k], pk[k] >> 16, mx) & 0xffu;
       if (mx ? uint32_t(a1[k]) < m : m < uint32_t(a1[k])) acc[k].v[0] = m;
+    }
+  }
+  const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int k = 0; k < kMaxReduceSpecs; ++k) {
+    if (k >= int(S.n)) break;
+    for (int d = 16; d > 0; d >>= 1) {
+      const Acc o = shfl_down(acc[k], d);
+      if (lane < uint32_t(d)) combine(S.s[k], acc[k], o);
+    }
+    if (lane == 0) warp_acc[warp][k] = acc[k];
+  }
+  __syncthreads();
+  if (threadIdx.x < uint32_t(S.n)) {
+    const int k = int(threadIdx.x);
+    Acc a = warp_acc[0][k];
+    for (uint32_t w = 1; w < kRBlock / 32; ++w) combine(S.s[k], a, warp_acc[w][k]);
+    partials[uint64_t(blockIdx.x) * kMaxReduceSpecs + k] = a;
+  }
+}
+
+// Plain u8x3 rows (interleaved 3-channel bytes): vectors of 16 pixels = 48
+// bytes (three 16-byte loads), the same cursor walk; per channel, Sum through
+// dp4a with the channel's byte mask (the channel pattern repeats every three
+// words), Max / Min on the extracted bytes.
+struct Px16 {
+  uint32_t w[12];
+};
+
+__device__ __forceinline__ Px16 plain3_load(const PlainRows& R, const PlainCursor& c, int& n) {
+  Px16 p;
+  const uint32_t left = R.width - c.xv * 16u;
+  const uint64_t a = R.base + c.off;
+  if (left >= 16u) {
+#pragma unroll
+    for (int i = 0; i < 3; ++i)
+      asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(p.w[4 * i]), "=r"(p.w[4 * i + 1]), "=r"(p.w[4 * i + 2]), "=r"(p.w[4 * i + 3])
+                   : "l"(a + 16u * i));
+    n = 16;
+  } else {
+#pragma unroll
+    for (int i = 0; i < 12; ++i) p.w[i] = 0;
+    for (uint32_t b = 0; b < 3 * left; ++b)
+      p.w[b >> 2] |= uint32_t(*reinterpret_cast<const uint8_t*>(a + b)) << (8 * (b & 3));
+    n = int(left);
+  }
+  return p;
+}
+
+__device__ __noinline__ Acc fold3_general(const DPlan& P, const RSpecDev& s, Acc a, Px16 p, int n) {
+  uint32_t w[16][3];
+#pragma unroll
+  for (int e = 0; e < 16; ++e)
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+      const int b = 3 * e + l;
+      w[e][l] = (p.w[b >> 2] >> (8 * (b & 3))) & 0xffu;
+    }
+  if (s.op != kNoOp) dev::run_ops(P, s.op, 1, 0, w);
+  fold_spec<uint32_t, 16, 3>(s, a, w, n);
+  return a;
+}
+
+__device__ __forceinline__ void fold3_fast(const RSpecDev& s, Acc& a, const Px16& p) {
+  if (s.combine == FK_REDUCE_SUM) {
+    // byte p = 4 i + b of the vector is channel p % 3; masks per (channel, i % 3)
+    constexpr uint32_t M[3][3] = {{0x01000001u, 0x00010000u, 0x00000100u},
+                                  {0x00000100u, 0x01000001u, 0x00010000u},
+                                  {0x00010000u, 0x00000100u, 0x01000001u}};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      uint32_t t = uint32_t(a.v[c]);
+#pragma unroll
+      for (int i = 0; i < 12; ++i) t = __dp4a(p.w[i], M[c][i % 3], t);
+      a.v[c] = t;
+    }
+  } else {
+    const bool mx = s.combine == FK_REDUCE_MAX;
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      uint32_t m = uint32_t(a.v[c]);
+#pragma unroll
+      for (int e = 0; e < 16; ++e) {
+        const int b = 3 * e + c;
+        const uint32_t x = (p.w[b >> 2] >> (8 * (b & 3))) & 0xffu;
+        m = mx ? max(m, x) : min(m, x);
+      }
+      a.v[c] = m;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kRBlock, 2) fk_reduce_plain3(const __grid_constant__ DPlan P,
+                                                                          const __grid_constant__ RSpecsDev S,
+                                                                          const __grid_constant__ PlainRows R,
+                                                                          Acc* partials) {
+  __shared__ Acc warp_acc[kRBlock / 32][kMaxReduceSpecs];
+  Acc acc[kMaxReduceSpecs];
+#pragma unroll
+  for (int k = 0; k < kMaxReduceSpecs; ++k) identity_acc(S.s[k], acc[k]);
+  const uint32_t total = R.vecs;
+  const uint32_t stride = gridDim.x * kRBlock;
+  uint32_t v = blockIdx.x * kRBlock + threadIdx.x;
+  if (v < total) {
+    const uint32_t sy = dev::fastdiv(stride, R.vdiv), sx = stride - sy * R.vpr;
+    const uint32_t dstep = sy * uint32_t(R.pitch) + sx * R.vb;
+    const uint32_t wrap = uint32_t(R.pitch) - R.vpr * R.vb;
+    PlainCursor c = plain_start(R, v);
+    for (; v < total; v += stride) {
+      int n;
+      const Px16 p = plain3_load(R, c, n);
+      plain_advance(R, c, sx, dstep, wrap);
+#pragma unroll
+      for (int k = 0; k < kMaxReduceSpecs; ++k) {
+        if (k >= int(S.n)) break;
+        const RSpecDev& s = S.s[k];
+        if (s.op == kNoOp && n == 16) fold3_fast(s, acc[k], p);
+        else acc[k] = fold3_general(P, s, acc[k], p, n);
+      }
     }
   }
   const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
@@ -557,6 +677,7 @@ cudaError_t launch_reduce_plain(const DPlan& P, const RSpecsDev& S, const PlainR
                                 uint32_t nblocks, uint64_t* out, cudaStream_t st) {
   Acc* parts = static_cast<Acc*>(scratch);
   if (R.kind == FK_U8) fk_reduce_plain<FK_U8><<<nblocks, kRBlock, 0, st>>>(P, S, R, parts);
+  else if (R.kind == FK_U8X3) fk_reduce_plain3<<<nblocks, kRBlock, 0, st>>>(P, S, R, parts);
   else fk_reduce_plain<FK_F32><<<nblocks, kRBlock, 0, st>>>(P, S, R, parts);
   fk_reduce_final<<<S.n, kRBlock, 0, st>>>(S, parts, nblocks, out);
   return cudaGetLastError();
@@ -565,6 +686,7 @@ cudaError_t launch_reduce_plain(const DPlan& P, const RSpecsDev& S, const PlainR
 uint32_t reduce_plain_blocks(uint32_t kind, int sms) {
   int per_sm = 0;
   if (kind == FK_U8) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk_reduce_plain<FK_U8>, kRBlock, 0);
+  else if (kind == FK_U8X3) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk_reduce_plain3, kRBlock, 0);
   else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fk_reduce_plain<FK_F32>, kRBlock, 0);
   return uint32_t(std::max(1, per_sm)) * uint32_t(sms);
 }

@@ -30,7 +30,7 @@ struct RSpecsDev {
   RSpecDev s[kMaxReduceSpecs];
 };
 
-// a plain read: one plane of single-lane u8 / f32 rows, 16-byte aligned, no
+// a plain read: one plane of u8 / f32 / u8x3 rows, 16-byte aligned, no
 // default values or folded unaries, walked as 16-byte vectors
 struct PlainRows {
   uint64_t base;   // address of element (0, 0)
@@ -38,7 +38,8 @@ struct PlainRows {
   uint32_t width;  // elements per row
   uint32_t vpr;    // vectors per row
   uint32_t vecs;   // rows * vpr (< 2^32)
-  uint32_t kind;   // FK_U8 / FK_F32
+  uint32_t kind;   // FK_U8 / FK_F32 (16-byte vectors) / FK_U8X3 (16 pixels, 48 bytes)
+  uint32_t vb;     // bytes per vector
   FastDiv vdiv;    // / vpr
 };
 

@@ -15,7 +15,7 @@ import pytest
 
 from fkchains import _rand_compute, make_compute, make_read, random_chain
 from paper_2508_07071_b200 import opfuse as of
-from paper_2508_07071_b200._ffi import F32, F64, F64X3, LANES, REDUCE_MAX, REDUCE_MIN, REDUCE_SUM, U8, U8X3
+from paper_2508_07071_b200._ffi import F32, F32X3, F64, F64X3, LANES, REDUCE_MAX, REDUCE_MIN, REDUCE_SUM, U8, U8X3
 from paper_2508_07071_b200.opfuse import Library, OpfuseError
 
 
@@ -182,31 +182,34 @@ def test_cuda_large_u8x3_and_many_specs(oracle):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("dt,kind", [(np.uint8, U8), (np.float32, F32)])
+@pytest.mark.parametrize("dt,kind", [(np.uint8, U8), (np.float32, F32), (np.uint8, U8X3)])
 def test_cuda_plain_rows(oracle, dt, kind):
-    """One plane of 16-byte aligned single-lane rows: the vector kernel
-    (fk_reduce_plain). Crops whose width is not a multiple of the vector leave a
-    partial last vector per row; transforms run per spec; -0 / NaN included."""
+    """One plane of 16-byte aligned u8 / f32 / u8x3 rows: the vector kernels
+    (fk_reduce_plain, fk_reduce_plain3). Crops whose width is not a multiple of
+    the vector leave a partial last vector per row; transforms run per spec;
+    -0 / NaN included; an unaligned crop takes the per-tile kernel."""
     cuda = Library("cuda")
     rng = np.random.default_rng(21)
-    big = (rng.integers(0, 256, (517, 1024), dtype=np.uint8) if dt == np.uint8
-           else rng.standard_normal((517, 1024)).astype(np.float32))
+    shape = (517, 1024, 3) if kind == U8X3 else (517, 1024)
+    big = (rng.integers(0, 256, shape, dtype=np.uint8) if dt == np.uint8
+           else rng.standard_normal(shape).astype(np.float32))
     if dt == np.float32:
         big[rng.random(big.shape) < 0.001] = np.nan
+    cast_to = {U8: F32, F32: U8, U8X3: F32X3}[kind]
+    vals = (3, 4, 5) if kind == U8X3 else (3,)
     crops = [(0, 0, 1024, 517), (16, 3, 37, 200), (16, 0, 1000, 1), (0, 1, 5, 516), (64, 5, 960, 511), (3, 2, 50, 50)]
     for x0, y0, w, h in crops:
         specs_of = lambda lib: [(REDUCE_SUM, None, None), (REDUCE_MAX, None, None), (REDUCE_MIN, None, None),  # noqa
-                                (REDUCE_SUM, lib.make_arith(8, of.const_of(kind, 3)), None),
-                                (REDUCE_MAX, lib.op_cast(kind, F32 if kind == U8 else U8), of.const_of(
-                                    F32 if kind == U8 else U8, 7))]
+                                (REDUCE_SUM, lib.make_arith(8, of.const_of(kind, *vals)), None),
+                                (REDUCE_MAX, lib.op_cast(kind, cast_to), of.const_of(cast_to, *([7] * len(vals))))]
         res = []
         for lib in (cuda, oracle):
-            p = lib.plane_from_numpy(big)
-            r = lib.op_crop(p, x0, y0, w, h) if (w, h) != big.shape[::-1] else lib.op_read_per_thread(p)
+            p = lib.plane_from_numpy(big, kind)
+            r = lib.op_crop(p, x0, y0, w, h) if (w, h) != (1024, 517) else lib.op_read_per_thread(p)
             res.append(lib.multi_reduce_plane(r, specs_of(lib)))
         assert res[0][1] == res[1][1] == w * h
-        if (x0, y0, w, h) == crops[0] or x0 % 16 == 0:
+        if x0 % 16 == 0:
             assert cuda.last_kernel().startswith("fk_reduce_plain"), cuda.last_kernel()
-        kinds = [kind, kind, kind, kind, F32 if kind == U8 else U8]
+        kinds = [kind, kind, kind, kind, cast_to]
         for x, y, (c, _, _), k in zip(res[0][0], res[1][0], specs_of(oracle), kinds):
             close(x, y, c, k)

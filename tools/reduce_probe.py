@@ -6,7 +6,7 @@ from paper_2508_07071_b200.opfuse import Library
 from paper_2508_07071_b200._ffi import REDUCE_SUM, REDUCE_MAX, REDUCE_MIN
 lib = Library("cuda")
 rng = np.random.default_rng(0)
-for shape, dt in (((2160, 3840), np.float32), ((8192, 8192), np.float32), ((1080, 1920, 3), np.uint8), ((8192, 8192), np.uint8)):
+for shape, dt in (((2160, 3840), np.float32), ((8192, 8192), np.float32), ((1080, 1920, 3), np.uint8), ((8192, 8192), np.uint8), ((4320, 7680, 3), np.uint8)):
     a = (rng.random(shape, dtype=np.float32) if dt == np.float32 else rng.integers(0, 256, shape, dtype=np.uint8))
     r = lib.op_read_per_thread(lib.plane_from_numpy(a))
     which = os.environ.get("SPECS", "sum,max,min").split(",")
