@@ -1162,7 +1162,11 @@ std::vector<Element> multi_reduce(const Op& read, const std::vector<ReduceSpecHo
       cuda_check(cudaMallocAsync(reinterpret_cast<void**>(&first), 6 * kMaxReduceSpecs * sizeof(unsigned long long), st),
                  "cudaMallocAsync");
       cuda_check(cudaMemsetAsync(first, 0xff, 6 * kMaxReduceSpecs * sizeof(unsigned long long), st), "cudaMemsetAsync");
-      cuda_check(launch_reduce_zero_sign(cls, P, S, zmask, nblocks, first, st), "fk_reduce_zero_sign launch");
+      if (plain && R.kind != FK_U8X3)
+        cuda_check(launch_reduce_plain_zero_sign(P, S, R, zmask, plain_blocks, first, st),
+                   "fk_reduce_plain_zero_sign launch");
+      else
+        cuda_check(launch_reduce_zero_sign(cls, P, S, zmask, nblocks, first, st), "fk_reduce_zero_sign launch");
       g_launches.fetch_add(1, std::memory_order_relaxed);
       unsigned long long hf[6 * kMaxReduceSpecs];
       cuda_check(cudaMemcpyAsync(hf, first, sizeof hf, cudaMemcpyDeviceToHost, st), "cudaMemcpyAsync");

@@ -569,6 +569,68 @@ __global__ void __launch_bounds__(kRBlock, 2) fk_reduce_plain3(const __grid_cons
   }
 }
 
+// Zero-sign pass over plain rows (u8 / f32 reads whose spec values are f32):
+// each thread keeps the first +0 / -0 it meets per flagged spec (its walk is
+// in increasing (y, x) order, and v * VE + e is monotone in it), then one
+// atomicMin per warp — no per-element atomics on zero-heavy planes.
+template <uint32_t KIND>
+__global__ void __launch_bounds__(kRBlock) fk_reduce_plain_zero_sign(const __grid_constant__ DPlan P,
+                                                                   const __grid_constant__ RSpecsDev S,
+                                                                   const __grid_constant__ PlainRows R,
+                                                                   uint32_t zmask, unsigned long long* first) {
+  constexpr int VE = KIND == FK_U8 ? 16 : 4;
+  unsigned long long f[kMaxReduceSpecs][2];
+#pragma unroll
+  for (int k = 0; k < kMaxReduceSpecs; ++k) f[k][0] = f[k][1] = ~0ull;
+  const uint32_t total = R.vecs;
+  const uint32_t stride = gridDim.x * kRBlock;
+  uint32_t v = blockIdx.x * kRBlock + threadIdx.x;
+  if (v < total) {
+    const uint32_t sy = dev::fastdiv(stride, R.vdiv), sx = stride - sy * R.vpr;
+    const uint32_t dstep = sy * uint32_t(R.pitch) + sx * R.vb;
+    const uint32_t wrap = uint32_t(R.pitch) - R.vpr * R.vb;
+    PlainCursor c = plain_start(R, v);
+    for (; v < total; v += stride) {
+      uint4 q;
+      const int n = plain_load<KIND>(R, c, q);
+      plain_advance(R, c, sx, dstep, wrap);
+      uint32_t x[VE][1];
+      const uint32_t qw[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+      for (int e = 0; e < VE; ++e) x[e][0] = KIND == FK_U8 ? (qw[e >> 2] >> (8 * (e & 3))) & 0xffu : qw[e];
+#pragma unroll
+      for (int k = 0; k < kMaxReduceSpecs; ++k) {
+        if (k >= int(S.n) || !((zmask >> (3 * k)) & 1u)) continue;
+        uint32_t w[VE][1];
+#pragma unroll
+        for (int e = 0; e < VE; ++e) w[e][0] = x[e][0];
+        if (S.s[k].op != kNoOp) dev::run_ops(P, S.s[k].op, 1, 0, w);
+#pragma unroll
+        for (int e = 0; e < VE; ++e) {
+          if (e < n && (w[e][0] & 0x7fffffffu) == 0) {
+            const unsigned long long i = uint64_t(v) * VE + e;
+            if (w[e][0] >> 31) f[k][1] = i < f[k][1] ? i : f[k][1];
+            else f[k][0] = i < f[k][0] ? i : f[k][0];
+          }
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kMaxReduceSpecs; ++k) {
+    if (k >= int(S.n) || !((zmask >> (3 * k)) & 1u)) continue;
+#pragma unroll
+    for (int sgn = 0; sgn < 2; ++sgn) {
+      unsigned long long m = f[k][sgn];
+      for (int d = 16; d > 0; d >>= 1) {
+        const unsigned long long o = __shfl_down_sync(0xffffffffu, m, d);
+        m = o < m ? o : m;
+      }
+      if ((threadIdx.x & 31u) == 0 && m != ~0ull) atomicMin(first + 6 * k + sgn, m);
+    }
+  }
+}
+
 // one CTA per spec: the CTA partials, then the spec's identity (the left-most
 // operand of the reference's merge, dpp.cpp:232-237) and finish_accum
 // (dpp.cpp:138-152). out: 3 lane words per spec (value kind bits).
@@ -680,6 +742,13 @@ cudaError_t launch_reduce_plain(const DPlan& P, const RSpecsDev& S, const PlainR
   else if (R.kind == FK_U8X3) fk_reduce_plain3<<<nblocks, kRBlock, 0, st>>>(P, S, R, parts);
   else fk_reduce_plain<FK_F32><<<nblocks, kRBlock, 0, st>>>(P, S, R, parts);
   fk_reduce_final<<<S.n, kRBlock, 0, st>>>(S, parts, nblocks, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_reduce_plain_zero_sign(const DPlan& P, const RSpecsDev& S, const PlainRows& R, uint32_t zmask,
+                                          uint32_t nblocks, unsigned long long* first, cudaStream_t st) {
+  if (R.kind == FK_U8) fk_reduce_plain_zero_sign<FK_U8><<<nblocks, kRBlock, 0, st>>>(P, S, R, zmask, first);
+  else fk_reduce_plain_zero_sign<FK_F32><<<nblocks, kRBlock, 0, st>>>(P, S, R, zmask, first);
   return cudaGetLastError();
 }
 

@@ -52,6 +52,9 @@ cudaError_t launch_reduce_zero_sign(int cls, const DPlan& P, const RSpecsDev& S,
                                     unsigned long long* first, cudaStream_t st);
 cudaError_t launch_reduce_plain(const DPlan& P, const RSpecsDev& S, const PlainRows& R, void* scratch,
                                 uint32_t nblocks, uint64_t* out, cudaStream_t st);
+// zero-sign pass over plain u8 / f32 rows (single-lane specs: zmask bits 3 * spec)
+cudaError_t launch_reduce_plain_zero_sign(const DPlan& P, const RSpecsDev& S, const PlainRows& R, uint32_t zmask,
+                                          uint32_t nblocks, unsigned long long* first, cudaStream_t st);
 uint32_t reduce_plain_blocks(uint32_t kind, int sms);  // resident CTAs on the device
 size_t reduce_scratch_bytes(uint32_t nblocks);
 int reduce_tile_elems();
