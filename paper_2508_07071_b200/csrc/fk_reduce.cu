@@ -682,6 +682,7 @@ template <class Lane, int L>
 __global__ void __launch_bounds__(kRBlock) fk_reduce_zero_sign(const __grid_constant__ DPlan P,
                                                              const __grid_constant__ RSpecsDev S, uint32_t zmask,
                                                              unsigned long long* first) {
+  uint32_t done = 0;  // (spec, lane, sign) keys this thread has already recorded
   const uint64_t total = uint64_t(P.tiles) * P.batch;
   const uint64_t stride = uint64_t(gridDim.x) * kRBlock;
   for (uint64_t t = uint64_t(blockIdx.x) * kRBlock + threadIdx.x; t < total; t += stride) {
@@ -701,7 +702,11 @@ __global__ void __launch_bounds__(kRBlock) fk_reduce_zero_sign(const __grid_cons
           const uint64_t mag = f32 ? (x.v[l] & 0x7fffffffu) : (x.v[l] & 0x7fffffffffffffffull);
           if (mag == 0) {
             const bool neg = f32 ? ((x.v[l] >> 31) & 1u) : ((x.v[l] >> 63) & 1u);
-            atomicMin(first + 6 * k + 2 * l + (neg ? 1 : 0), (unsigned long long)(i0 + e));
+            const uint32_t bit = 1u << (6 * k + 2 * l + (neg ? 1 : 0));
+            if (!(done & bit)) {  // the thread walks in increasing (z, y, x): its first is its minimum
+              atomicMin(first + 6 * k + 2 * l + (neg ? 1 : 0), (unsigned long long)(i0 + e));
+              done |= bit;
+            }
           }
         }
       }
