@@ -1113,6 +1113,10 @@ fk_status fk_multi_reduce_plane(const fk_iop* read, const fk_reduce_spec* specs,
   elem_t* ident = (elem_t*)calloc(n, sizeof(elem_t));
   for (uint32_t s = 0; s < n; ++s) {
     const fk_iop* t = specs[s].transform;
+    if (specs[s].combine > FK_REDUCE_MIN) {  /* C-ABI enum check (fk.h: FK_E_INVALID_ARGUMENT) */
+      free(vkind); free(ident);
+      return fail(FK_E_INVALID_ARGUMENT, -1, "reduce spec: unknown combine");
+    }
     if (t) {
       if (t->opkind != FK_KIND_UNARY && t->opkind != FK_KIND_BINARY) {
         free(vkind); free(ident);

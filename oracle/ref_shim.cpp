@@ -397,6 +397,8 @@ extern "C" fk_status fk_multi_reduce_plane(const fk_iop* read, const fk_reduce_s
                                            int32_t workers, void* results, uint64_t* elements_read) {
   if (!read || (!specs && n) || (!results && n))
     return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: null argument");
+  for (uint32_t i = 0; i < n; ++i)  // the C-ABI's enum check (the reference's Reducer is a C++ enum)
+    if (specs[i].combine > FK_REDUCE_MIN) return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: unknown combine");
   try {
     for (auto& b : read->srcs) copy_in(*b);
     std::vector<ReduceSpec> rs(n);

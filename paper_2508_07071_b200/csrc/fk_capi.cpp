@@ -244,6 +244,7 @@ fk_status fk_multi_reduce_plane(const fk_iop* read, const fk_reduce_spec* specs,
     if (n && (!specs || !results)) fk::fail(FK_E_INVALID_ARGUMENT, "null specs / results");
     std::vector<fk::ReduceSpecHost> hs(n);
     for (uint32_t i = 0; i < n; ++i) {
+      if (specs[i].combine > FK_REDUCE_MIN) fk::fail(FK_E_INVALID_ARGUMENT, "reduce spec: unknown combine");
       hs[i].transform = specs[i].transform ? &specs[i].transform->op : nullptr;
       hs[i].combine = specs[i].combine;
       hs[i].has_identity = specs[i].has_identity != 0;

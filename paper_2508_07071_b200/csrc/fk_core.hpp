@@ -10,6 +10,7 @@
 #include <array>
 #include <cstdint>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <optional>
 #include <stdexcept>
@@ -109,9 +110,11 @@ struct Pipeline {
   std::vector<Op> compute;
   Op write;
   fk_extent3 space{};
-  // device-side program, built and uploaded once on first execute (the paper's
-  // "compute the CPU part once")
-  std::shared_ptr<DeviceProgram> dev;
+  // device-side programs, one per CUDA device, each built and uploaded once on
+  // the first execute on that device (the paper's "compute the CPU part once",
+  // PAPER.md:701-703) and kept for the pipeline's lifetime: executes on other
+  // devices never replace it (guarded by fk_exec.cu's build mutex)
+  std::map<int, std::shared_ptr<DeviceProgram>> dev;
   ~Pipeline();
 };
 

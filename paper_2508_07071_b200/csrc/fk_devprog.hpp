@@ -112,11 +112,9 @@ struct DPlan {
   uint32_t slots_per_cta;    // 1, or 2 planes sharing one row/visit table (equal rect_h, mode, swap)
   uint32_t slot_threads;     // threads per plane slot
   uint32_t slices;           // CTA slices along z (slots != nullptr)
-  uint32_t no_stage;         // 1: column-streaming kernel uses direct tap loads (A/B; FK_SEP_NOSTAGE=1)
+  uint32_t no_stage;         // 1: column-streaming kernel uses direct tap loads (spans the ring cannot hold)
   uint32_t dir_rep[4];       // fk_direct: repeat count of chain op k (its constant / reciprocal in aff_c / aff_r [k][0])
   FastDiv zdiv;              // fk_reduce: n / tiles (plane of a linear tile index)
-  uint32_t ring_span;        // fk_resample_tma: ring bytes per plane slot (16-byte multiple)
-  uint32_t no_bulk;          // 1 (default): the staged walk uses per-lane cp.async; 0: per-warp bulk copies (FK_SEP_BULK=1)
 };
 constexpr uint32_t kNoPlane = 0xffffffffu;
 

@@ -336,16 +336,25 @@ int recip_div_verified(float d) {
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
   }
+  // fails closed: any CUDA error leaves the divisor unverified (0, the
+  // guarded __fdiv_rn path) and is not cached, so a later call retries
   unsigned int* flag = nullptr;
   int ok = 0;
+  bool clean = false;
   if (cudaMalloc(&flag, sizeof(unsigned int)) == cudaSuccess) {
-    cudaMemset(flag, 0, sizeof(unsigned int));
-    fk_verify_recip_div<<<148 * 16, 256>>>(d, flag);
-    unsigned int h = 3;
-    if (cudaMemcpy(&h, flag, sizeof h, cudaMemcpyDeviceToHost) == cudaSuccess) ok = (h & 1u) ? 0 : ((h & 2u) ? 1 : 2);
+    if (cudaMemset(flag, 0, sizeof(unsigned int)) == cudaSuccess) {
+      fk_verify_recip_div<<<148 * 16, 256>>>(d, flag);
+      unsigned int h = 3;
+      if (cudaGetLastError() == cudaSuccess &&
+          cudaMemcpy(&h, flag, sizeof h, cudaMemcpyDeviceToHost) == cudaSuccess) {
+        ok = (h & 1u) ? 0 : ((h & 2u) ? 1 : 2);
+        clean = true;
+      }
+    }
     cudaFree(flag);
   }
   cudaGetLastError();
+  if (!clean) return 0;
   std::lock_guard<std::mutex> lock(mu);
   cache[key] = ok;
   return ok;

@@ -20,6 +20,7 @@
 #include <tuple>
 
 #include "fk_core.hpp"
+#include "fk_crop.hpp"
 #include "fk_reduce.hpp"
 #include "fk_exec.hpp"
 #include "fk_launch.hpp"
@@ -186,9 +187,7 @@ struct DeviceProgram {
   uint32_t* d_order = nullptr;   // plane visiting order (grouped by source), or null
   uint32_t* d_slots2 = nullptr;  // column-streaming kernel: planes paired by (mode, rect_h, swap), kNoPlane = none
   uint32_t n_slices2 = 0;        // ... number of pairs
-  int stage_ok[2] = {-1, -1};    // staged column walk valid for [single, dual] slices (-1: not yet computed)
-  int tma_ok[2] = {-1, -1};      // bulk-copy producer/consumer walk valid for [single, dual] slices
-  uint32_t tma_span[2] = {0, 0}; // ... its ring bytes per plane slot
+  bool stage_ok[2] = {false, false};  // staged column walk valid for [single, dual] slices (set at build)
   std::vector<void*> extra;      // BatchArith constant tables
   std::vector<DSample> reads;    // host copies
   bool read_flat = false, write_flat = false;
@@ -199,6 +198,11 @@ struct DeviceProgram {
   uint64_t def[3] = {0, 0, 0};
   uint32_t def_kind = 0;
   Traffic traffic;               // analytic ExecReport counters (computed once)
+  // planar crop kernel (fk_crop.cu): crop -> bilinear -> [swap] -> f32 chain -> split f32
+  bool crop_ok = false;
+  bool crop_perz = false;        // per-plane chain constants (BatchArith or per-plane lane swaps)
+  uint32_t crop_sig = 0;
+  CropPlan crop{};               // tables, order, inline constants (reads / writes set at launch)
 
   ~DeviceProgram() {
     for (void* p : {static_cast<void*>(d_table), static_cast<void*>(d_reads), static_cast<void*>(d_writes),
@@ -283,6 +287,243 @@ void keep_pool_memory(int device) {
   cudaGetLastError();
   done.push_back(device);
 }
+
+
+// ------------------------------------------------------ planar crop kernel --
+// floor(a / b) for b > 0
+int64_t floor_div(int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
+
+// CropRow for output row y (fk_crop.hpp): center_coord / floor / clamp of
+// ops.cpp:253-275 in exact integers, and the dp2a weights of the vertical lerp.
+CropRow crop_row(uint32_t y, uint32_t rect_h, uint32_t out_h) {
+  const int64_t den = 2 * int64_t(out_h);
+  const int64_t P = (2 * int64_t(y) + 1) * rect_h - out_h;
+  const int64_t iy = floor_div(P, den), ny = P - iy * den;
+  const int64_t maxy = int64_t(rect_h) - 1;
+  const uint32_t iy0 = uint32_t(std::min(std::max<int64_t>(iy, 0), maxy));
+  const uint32_t iy1 = uint32_t(std::min(std::max<int64_t>(iy + 1, 0), maxy));
+  CropRow r{};
+  uint32_t K, d, n;
+  const bool exact = (ny * 64) % den == 0;  // fy a multiple of 1/64: den 64, K 256, every FP32 step exact
+  if (exact) {
+    d = 64; n = uint32_t(ny * 64 / den); K = 256;
+  } else {
+    d = uint32_t(den); n = uint32_t(ny); K = uint32_t(8388607 / (255 * den));  // K d 255 < 2^23
+  }
+  r.iy = iy0 | (iy1 << 16) | (exact ? kCropExact : 0u);
+  r.wts = (K * (d - n)) | ((K * n) << 16);
+  r.s = float(64.0 / (double(K) * d));
+  r.c = -131072.0f * r.s;  // exact: a power-of-two multiple
+  return r;
+}
+
+// CropCol for output column x: left tap (relative, clamped) and the reference's
+// fx (cx - floor(cx) in double, ops.cpp:262-266) rounded to f32; 0 where both
+// taps clamp to one column.
+CropCol crop_col(uint32_t x, uint32_t rect_w, uint32_t out_w) {
+  const int64_t den = 2 * int64_t(out_w);
+  const int64_t P = (2 * int64_t(x) + 1) * rect_w - out_w;
+  const int64_t ix = floor_div(P, den), nx = P - ix * den;
+  const int64_t maxx = int64_t(rect_w) - 1;
+  CropCol c{};
+  if (ix < 0 || ix + 1 > maxx) {
+    c.ix = uint32_t(ix < 0 ? 0 : maxx) | kCropExact;
+    c.fx = 0.0f;
+    return c;
+  }
+  const double cx = (double(x) + 0.5) * double(rect_w) / double(out_w) - 0.5;
+  c.ix = uint32_t(ix) | ((nx * 256) % den == 0 ? kCropExact : 0u);
+  c.fx = float(cx - std::floor(cx));
+  return c;
+}
+
+// Two-op division q = fma(x, r_hi, RN(x r_lo)): equal to IEEE x / d on every value op k of
+// the AFFINE chain can receive (prefix_k of the 256 u8 values, per lane and plane)?
+bool recip2_div_exact(const std::vector<DOp>& arith, size_t k, const std::map<uint64_t, std::vector<uint64_t>>& rows,
+                      uint32_t batch) {
+  bool per_plane = false;
+  for (size_t j = 0; j <= k; ++j) per_plane = per_plane || arith[j].per_z;
+  const uint32_t planes = per_plane ? batch : 1;
+  auto lane_const = [&](const DOp& d, uint32_t z, int l) {
+    const int li = d.nl == 3 ? l : 0;
+    if (!d.per_z) return f32_bits(d.c[li]);
+    const std::vector<uint64_t>& r = rows.at(d.per_z);
+    return f32_bits(r[3 * size_t(z < d.per_z_n ? z : d.per_z_n - 1) + li]);
+  };
+  for (uint32_t z = 0; z < planes; ++z)
+    for (int l = 0; l < 3; ++l) {
+      const float d = lane_const(arith[k], z, l);
+      const float rh = 1.0f / d;
+      const float rl = float(1.0 / double(d) - double(rh));
+      for (int t = 0; t < 256; ++t) {
+        float v = float(t);
+        for (size_t j = 0; j < k; ++j) {
+          const float c = lane_const(arith[j], z, l);
+          switch (arith[j].fn) {
+            case AF_MUL: v = v * c; break;
+            case AF_ADD: v = v + c; break;
+            case AF_SUB: v = v - c; break;
+            default: v = v / c; break;
+          }
+        }
+        if (!same_f32(std::fmaf(v, rh, v * rl), v / d)) return false;
+      }
+    }
+  return true;
+}
+
+// Eligibility, tables and constants of the planar crop kernel: every plane a
+// bilinear crop of a u8x3 frame (4-byte aligned rows), an AFFINE chain, a
+// split write of three f32 planes with one 16-byte multiple pitch.
+void build_crop(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& arith, uint32_t sig,
+                const std::vector<DWrite>& writes) {
+  const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
+  const uint32_t wid = p.write.id == FK_OP_BATCH_WRITE ? p.write.w_inner : p.write.id;
+  if (!dp.affine_ok || dp.resample_lanes != 3 || wid != FK_OP_SPLIT_WRITE || B == 0 || W % 4 || W / 4 > kCropMaxQuads ||
+      W == 0 || H == 0 || H > 16448 || lane_kind(uint32_t(p.write.in_kind)) != FK_F32)
+    return;
+  bool ok = true;
+  for (const DSample& s : dp.reads)
+    ok = ok && s.mode == RD_BILINEAR && s.kind == FK_U8X3 && !(s.flags & SF_DEFAULT) && s.rect_h < 32768 &&
+         s.rect_w < (1u << 30) && ((s.src | s.pitch) & 15) == 0 && s.pitch < (1ull << 32) && s.out_w == W &&
+         s.out_h == H;
+  for (const DWrite& w : writes)
+    ok = ok && (w.flags & WF_ACTIVE) && w.pitch[0] == w.pitch[1] && w.pitch[0] == w.pitch[2] &&
+         (w.pitch[0] & 15) == 0 && w.pitch[0] < (1ull << 32) && ((w.dst[0] | w.dst[1] | w.dst[2]) & 15) == 0;
+  if (!ok) return;
+  // chain: the AFFINE signature with the verified division forms
+  uint32_t fn[4] = {0, 0, 0, 0}, fast = 0, two = 0;
+  for (size_t k = 0; k < arith.size(); ++k) {
+    fn[k] = arith[k].fn;
+    if (fn[k] != AF_DIV) continue;
+    if (recip2_div_exact(arith, k, dp.per_z_host, B)) two |= 1u << k;
+    else if (sig_fast(sig, int(k))) fast |= 1u << k;
+  }
+  uint32_t csig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast) | (two << kCropDiv2);
+  if (!crop_registered(csig)) csig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast);
+  if (!crop_registered(csig)) csig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], 0);
+  if (!crop_registered(csig)) return;
+  // row bands: enough CTAs for ~2 waves of 4 per SM on small batches
+  const uint64_t target = 148ull * 4 * 2;
+  uint32_t bands = B >= target ? 1u
+                               : uint32_t(std::min<uint64_t>((target + B - 1) / B, (H + kCropTileRows - 1) / kCropTileRows));
+  uint32_t band_rows = (H + bands - 1) / bands;
+  band_rows = (band_rows + kCropTileRows - 1) / kCropTileRows * kCropTileRows;
+  bands = (H + band_rows - 1) / band_rows;
+  // tables: one per distinct crop height / width (out extents are uniform)
+  std::vector<CropRow> rows;
+  std::vector<CropCol> cols;
+  std::map<uint32_t, uint32_t> row_at, col_at;
+  std::vector<CropAux> aux(B);
+  uint32_t max_words = 0, max_stage = 0;
+  bool swap0 = false, swap_uniform = true;
+  for (uint32_t z = 0; z < B; ++z) {
+    const DSample& s = dp.reads[z];
+    auto r = row_at.find(s.rect_h);
+    if (r == row_at.end()) {
+      r = row_at.emplace(s.rect_h, uint32_t(rows.size())).first;
+      for (uint32_t y = 0; y < H; ++y) rows.push_back(crop_row(y, s.rect_h, H));
+      // source rows a tile stages: [iy0 of its first row, iy1 of its last]
+      for (uint32_t b = 0; b < bands; ++b)
+        for (uint32_t ty = b * band_rows; ty < std::min(H, (b + 1) * band_rows); ty += kCropTileRows) {
+          const uint32_t ly = std::min({H, (b + 1) * band_rows, ty + kCropTileRows}) - 1;
+          const uint32_t lo = rows[r->second + ty].iy & 0x7fffu, hi = (rows[r->second + ly].iy >> 16) & 0x7fffu;
+          max_stage = std::max(max_stage, hi - lo + 1);
+        }
+    }
+    auto c = col_at.find(s.rect_w);
+    if (c == col_at.end()) {
+      c = col_at.emplace(s.rect_w, uint32_t(cols.size())).first;
+      for (uint32_t x = 0; x < W; ++x) cols.push_back(crop_col(x, s.rect_w, W));
+    }
+    CropAux& a = aux[z];
+    a.rowtab = r->second;
+    a.coltab = c->second;
+    const uint32_t first = s.x0 + (cols[c->second].ix & ~kCropExact);
+    const uint32_t last = s.x0 + (cols[c->second + W - 1].ix & ~kCropExact) + 1;  // + the right tap
+    a.wb = (3 * first) & ~15u;
+    a.nwords = ((3 * (last + 1) - a.wb + 15) / 16) * 4;
+    // the crop's last row may be the frame's last: staging zero-fills past its readable bytes
+    // (every real byte, < 3 (x0 + rect_w), is readable)
+    if (uint64_t(3) * (s.x0 + s.rect_w) > s.tail_bytes) return;
+    a.rlim = s.tail_bytes > a.wb ? s.tail_bytes - a.wb : 0u;
+    a.swap = (((s.flags & SF_POST_SWAP) != 0) != dp.fused_swap) ? 1u : 0u;
+    if (z == 0) swap0 = a.swap;
+    swap_uniform = swap_uniform && a.swap == uint32_t(swap0);
+    a.kz = z;
+    max_words = std::max(max_words, a.nwords);
+  }
+  const uint32_t v_stride = max_words * 16, stage_stride = max_words * 4;
+  if (crop_smem_bytes(v_stride, max_stage, stage_stride, W / 4) > 200 * 1024) return;
+  bool perz = !swap_uniform;
+  for (const DOp& d : arith) perz = perz || d.per_z;
+  // constants, input-lane order: lane m of plane z uses output lane sigma_z(m)
+  auto lane_const = [&](const DOp& d, uint32_t z, int l) {
+    const int li = d.nl == 3 ? l : 0;
+    if (!d.per_z) return f32_bits(d.c[li]);
+    const std::vector<uint64_t>& r = dp.per_z_host.at(d.per_z);
+    return f32_bits(r[3 * size_t(z < d.per_z_n ? z : d.per_z_n - 1) + li]);
+  };
+  auto consts = [&](size_t k, uint32_t z, int m, bool swap, float& c, float& h, float& l) {
+    c = lane_const(arith[k], z, swap ? 2 - m : m);
+    h = l = 0.0f;
+    if (arith[k].fn != AF_DIV) return;
+    h = 1.0f / c;
+    l = (two >> k) & 1u ? float(1.0 / double(c) - double(h)) : -c;
+  };
+  CropPlan& P = dp.crop;
+  P = CropPlan{};
+  if (perz) {
+    std::vector<float4> kz(size_t(B) * 12, make_float4(0, 0, 0, 0));
+    for (uint32_t z = 0; z < B; ++z)
+      for (size_t k = 0; k < arith.size(); ++k)
+        for (int m = 0; m < 3; ++m) {
+          float c, h, l;
+          consts(k, z, m, aux[z].swap != 0, c, h, l);
+          kz[size_t(z) * 12 + 3 * k + m] = make_float4(c, h, l, 0.0f);
+        }
+    P.kz = upload(kz);
+    dp.extra.push_back(const_cast<float4*>(P.kz));
+  } else {
+    for (size_t k = 0; k < arith.size(); ++k)
+      for (int m = 0; m < 3; ++m) {
+        float c, h, l;
+        consts(k, 0, m, swap0, c, h, l);
+        P.kc[k][m] = make_float2(c, c);
+        P.kh[k][m] = make_float2(h, h);
+        P.kl[k][m] = make_float2(l, l);
+      }
+  }
+  // visiting order: crops of one source frame back to back (the frame stays
+  // L2-resident while its crops run), widest spans first within a frame
+  std::vector<uint32_t> order(B);
+  for (uint32_t z = 0; z < B; ++z) order[z] = z;
+  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
+    if (dp.reads[a].src != dp.reads[b].src) return dp.reads[a].src < dp.reads[b].src;
+    return aux[a].nwords > aux[b].nwords;
+  });
+  P.aux = upload(aux);
+  P.rows = upload(rows);
+  P.cols = upload(cols);
+  P.order = upload(order);
+  for (const void* q : {static_cast<const void*>(P.aux), static_cast<const void*>(P.rows),
+                        static_cast<const void*>(P.cols), static_cast<const void*>(P.order)})
+    dp.extra.push_back(const_cast<void*>(q));
+  P.out_w = W;
+  P.out_h = H;
+  P.quads = W / 4;
+  P.v_stride = v_stride;
+  P.stage_rows = max_stage;
+  P.stage_stride = stage_stride;
+  P.n_planes = B;
+  P.bands = bands;
+  P.band_rows = band_rows;
+  dp.crop_ok = true;
+  dp.crop_perz = perz;
+  dp.crop_sig = csig;
+}
+
+bool sep_stage_ok(const DeviceProgram& dp, uint32_t W, uint32_t T, uint32_t spc);
 
 std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
   keep_pool_memory(device);
@@ -481,6 +722,7 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
         }
       }
     }
+    build_crop(*dp, p, arith, sig, writes);
   }
   // direct f32 kernel: f32 planes read as-is, f32 arith runs (any repeat), an
   // optional final Cast f32 -> u8, a packed write
@@ -562,6 +804,11 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
       dp->d_slots2 = upload(slots);
     }
   }
+  if (dp->resample_ok && dp->sep_ok) {  // staged column walk: every warp's span fits the ring
+    const uint32_t pairs = (W + 1) / 2;
+    dp->stage_ok[0] = sep_stage_ok(*dp, W, pairs, 1);
+    dp->stage_ok[1] = dp->d_slots2 != nullptr && sep_stage_ok(*dp, W, pairs, 2);
+  }
   dp->traffic = analytic_traffic(p);
   dp->d_table = upload(dp->table);
   dp->d_reads = upload(dp->reads);
@@ -614,11 +861,16 @@ int current_device() {
 
 std::mutex g_build_mu;
 
+// The pipeline's program for the current device, built on first use. The
+// returned reference stays valid for the pipeline's lifetime: programs are
+// never replaced, and all lazily derived plan state is computed in
+// build_program under this lock (execute_* only read it, so concurrent
+// executes of one pipeline are safe).
 DeviceProgram& ensure_program(const Pipeline& p) {
   const int dev = current_device();
   std::lock_guard<std::mutex> lock(g_build_mu);
-  auto& slot = const_cast<Pipeline&>(p).dev;
-  if (!slot || slot->device != dev) slot = build_program(p, dev);
+  auto& slot = const_cast<Pipeline&>(p).dev[dev];
+  if (!slot) slot = build_program(p, dev);
   return *slot;
 }
 
@@ -673,26 +925,6 @@ void fill_plan_io(DPlan& P, const DeviceProgram& dp, const Pipeline& p, const fk
 
 bool lut_allowed(const fk_exec_config* cfg) { return !(cfg && (cfg->flags & FK_EXEC_NO_LUT)); }
 
-// FK_PREFER_LUT=1 runs u8 AFFINE chains through the 256-entry table instead
-// (A/B profiling of LDS lookups vs in-register FP32 ops).
-bool lut_preferred() {
-  static const bool on = [] {
-    const char* e = std::getenv("FK_PREFER_LUT");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
-// FK_RESAMPLE_TILES=1 selects the earlier tile-per-thread resample kernel
-// (fk_resample.cu) instead of the column-streaming one, for A/B profiling.
-bool tile_resample() {
-  static const bool on = [] {
-    const char* e = std::getenv("FK_RESAMPLE_TILES");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
-
 }  // namespace
 
 namespace {
@@ -734,30 +966,6 @@ bool sep_stage_ok(const DeviceProgram& dp, uint32_t W, uint32_t T, uint32_t spc)
   return true;
 }
 
-// Can the bulk-copy (TMA) producer/consumer walk run? Bilinear planes with
-// 16-byte aligned rows, one CTA of <= 256 threads per slice, and each plane's
-// 16-byte rounded span inside the source view (DSample::tail_bytes). Returns the
-// ring bytes per plane slot, 0 when not applicable.
-uint32_t sep_tma_span(const DeviceProgram& dp, uint32_t W, uint32_t T, uint32_t spc, uint32_t slices) {
-  if (32 * ((spc * T + 31) / 32 + 1) > 256 || slices > 65535) return 0;
-  uint32_t span = 0;
-  const uint32_t c1 = std::min(2 * T, W);
-  for (const DSample& s : dp.reads) {
-    if (s.flags & SF_DEFAULT) continue;
-    if (s.mode != RD_BILINEAR) return 0;
-    if (((s.src + uint64_t(s.y0) * s.pitch) | s.pitch) & 15) return 0;
-    const uint32_t bpe = uint32_t(lanes_of(s.kind));
-    uint32_t lo, x1, x2, hi;
-    host_taps(s, 0, bpe, lo, x1);
-    host_taps(s, c1 - 1, bpe, x2, hi);
-    lo &= ~15u;
-    const uint32_t bytes = (hi + bpe - lo + 15) & ~15u;
-    if (uint64_t(lo) + bytes > s.tail_bytes) return 0;
-    span = std::max(span, bytes);
-  }
-  return span <= 4096 ? span : 0;
-}
-
 }  // namespace
 
 void check_config(const fk_exec_config* c) {  // executor.cpp:20-25
@@ -779,7 +987,7 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
   const bool generic_only = cfg && (cfg->flags & FK_EXEC_FORCE_GENERIC);
   // kernel selection: a registered compiled chain first, the interpreter otherwise
   const bool direct = dp.direct_ok && !generic_only;
-  const bool affine = !direct && dp.affine_ok && !generic_only && !lut_preferred();
+  const bool affine = !direct && dp.affine_ok && !generic_only;
   const bool compiled = affine || (!direct && dp.resample_ok && lut_allowed(cfg) && !generic_only);
   const int cls = generic_state_class(dp.fused_wide, dp.fused_lanes);
   DPlan P = base_plan(p.space.width, p.space.height, p.space.batch, dp.read_flat && dp.write_flat,
@@ -806,7 +1014,17 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     r.path = FK_PATH_COMPILED;
-  } else if (compiled && dp.sep_ok && !tile_resample()) {
+  } else if (affine && dp.crop_ok) {
+    // planar crop kernel: one CTA per (plane, row band), vertical-first two-phase tiles
+    CropPlan C = dp.crop;
+    C.reads = dp.d_reads;
+    C.writes = dp.d_writes;
+    cuda_check(launch_crop(dp.crop_sig, dp.crop_perz, C, C.n_planes * C.bands, st), "fk_crop launch");
+    t_last_kernel = "fk_crop";
+    ++r.kernels_launched;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    r.path = FK_PATH_COMPILED;
+  } else if (compiled && dp.sep_ok) {
     // column-streaming kernel: one warp per CTA, 32 column pairs x a band of rows
     // of one z slice (one plane, or two planes of equal row structure side by side)
     const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
@@ -820,18 +1038,7 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
     S.slots_per_cta = dual ? 2u : 1u;
     S.slot_threads = pairs;
     S.slices = dual ? dp.n_slices2 : B;
-    int& stage_ok = dp.stage_ok[dual ? 1 : 0];
-    if (stage_ok < 0) stage_ok = sep_stage_ok(dp, W, pairs, dual ? 2u : 1u) ? 1 : 0;
-    static const bool no_stage = [] {
-      const char* e = std::getenv("FK_SEP_NOSTAGE");
-      return e && e[0] == '1';
-    }();
-    S.no_stage = no_stage ? 1u : 0u;
-    static const bool no_bulk = [] {  // opt-in: per-warp bulk copies measured slower than cp.async on C5
-      const char* e = std::getenv("FK_SEP_BULK");
-      return !(e && e[0] == '1');
-    }();
-    S.no_bulk = no_bulk ? 1u : 0u;
+    S.no_stage = dp.stage_ok[dual ? 1 : 0] ? 0u : 1u;
     // band: whole planes (up to the table size) unless the batch is too small to
     // give ~2 waves of 16 warps per SM
     const uint64_t units = uint64_t(dual ? w2 : w1) * S.slices;
@@ -849,27 +1056,10 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
     S.width = W;
     S.height = H;
     S.tiles_per_cta = uint32_t(band);
-    static const bool no_tma = [] {  // the bulk-copy variant is opt-in (slower on C5, see fk_resample_sep.cuh)
-      const char* e = std::getenv("FK_SEP_TMA");
-      return !(e && e[0] == '1');
-    }();
-    int& tma_ok = dp.tma_ok[dual ? 1 : 0];
-    if (tma_ok < 0) {
-      dp.tma_span[dual ? 1 : 0] = sep_tma_span(dp, W, pairs, dual ? 2u : 1u, S.slices);
-      tma_ok = dp.tma_span[dual ? 1 : 0] ? 1 : 0;
-    }
-    if (tma_ok == 1 && !no_tma && !no_stage) {
-      S.ring_span = dp.tma_span[dual ? 1 : 0];
-      cuda_check(launch_resample_tma(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)),
-                                     P.write_mode == WR_SPLIT, affine ? dp.aff_sig : kSigLut, S, st),
-                 "fk_resample_tma launch");
-      t_last_kernel = "fk_resample_tma";
-    } else {
-      cuda_check(launch_resample_sep(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)), P.write_mode == WR_SPLIT,
-                                     affine ? dp.aff_sig : kSigLut, S, stage_ok == 1 && !S.no_stage, st),
-                 "fk_resample_sep launch");
-      t_last_kernel = "fk_resample_sep";
-    }
+    cuda_check(launch_resample_sep(dp.resample_lanes, lane_kind(uint32_t(p.write.in_kind)), P.write_mode == WR_SPLIT,
+                                   affine ? dp.aff_sig : kSigLut, S, S.no_stage == 0, st),
+               "fk_resample_sep launch");
+    t_last_kernel = "fk_resample_sep";
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     r.path = FK_PATH_COMPILED;
@@ -1085,8 +1275,6 @@ std::vector<Element> multi_reduce(const Op& read, const std::vector<ReduceSpecHo
   // the vector kernel (resident CTAs only, grid-stride)
   PlainRows R{};
   bool plain = false;
-  if (std::getenv("FK_DEBUG_REDUCE"))
-    std::fprintf(stderr, "reduce batch=%u cls=%d reads=%zu\n", sp.batch, cls, dp.reads.size());
   if (sp.batch == 1 && !dp.reads.empty() && (cls == 0 || (cls == 1 && dp.reads[0].kind == FK_U8X3))) {
     const DSample& r = dp.reads[0];
     const uint32_t ve = r.kind == FK_F32 ? 4u : 16u, eb = r.kind == FK_F32 ? 4u : (r.kind == FK_U8X3 ? 3u : 1u);
@@ -1094,12 +1282,7 @@ std::vector<Element> multi_reduce(const Op& read, const std::vector<ReduceSpecHo
     const uint64_t vpr = (uint64_t(sp.width) + ve - 1) / ve;
     plain = r.mode == RD_DIRECT && !(r.flags & SF_DEFAULT) && r.post_len == 0 &&
             (r.kind == FK_U8 || r.kind == FK_F32 || r.kind == FK_U8X3) && base % 16 == 0 && r.pitch % 16 == 0 &&
-            vpr * sp.height < (uint64_t(1) << 31) && r.pitch * sp.height < (uint64_t(1) << 32) &&
-            std::getenv("FK_REDUCE_GENERIC") == nullptr;
-    if (std::getenv("FK_DEBUG_REDUCE"))
-      std::fprintf(stderr, "reduce plain=%d mode=%u flags=%x post=%u kind=%u base%%16=%llu pitch=%llu vpr=%llu\n",
-                   int(plain), r.mode, r.flags, r.post_len, r.kind, (unsigned long long)(base % 16),
-                   (unsigned long long)r.pitch, (unsigned long long)vpr);
+            vpr * sp.height < (uint64_t(1) << 31) && r.pitch * sp.height < (uint64_t(1) << 32);
     if (plain) {
       R.base = base;
       R.pitch = r.pitch;

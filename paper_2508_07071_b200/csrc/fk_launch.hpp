@@ -34,11 +34,6 @@ uint32_t resample_sep_band_max();
 cudaError_t launch_resample_sep(int src_lanes, uint32_t out_lane_kind, bool split, uint32_t sig, const DPlan& P,
                                 bool staged, cudaStream_t st);
 uint32_t resample_sep_ring_row();
-// bulk-copy producer/consumer variant (bilinear planes, host-checked spans; P.ring_span set)
-cudaError_t launch_resample_tma(int src_lanes, uint32_t out_lane_kind, bool split, uint32_t sig, const DPlan& P,
-                                cudaStream_t st);
-uint32_t resample_tma_ring();
-size_t resample_tma_fix_bytes();
 
 bool resample_affine_registered(uint32_t sig);  // fk_sig.cuh FK_AFFINE_SIGS
 // sig == kSigLut: LUT mode; else the registered AFFINE chain signature

@@ -424,7 +424,11 @@ __global__ void __launch_bounds__(kRBlock, FK_PLAIN_MINB) fk_reduce_plain(const 
   for (int k = 0; k < kMaxReduceSpecs; ++k) {
     acc[k].v[0] = a1[k];
     acc[k].v[1] = acc[k].v[2] = 0;
-    if (KIND == FK_U8 && S.s[k].combine != FK_REDUCE_SUM) {  // the packed lanes' extremum joins the scalar one
+    // the packed lanes' extremum joins the scalar one — only for specs that fed
+    // them (u8 values, no transform: fold_vector_fast); any other spec's pk is
+    // an untouched seed (e.g. 0 for an f32 Min's +inf identity)
+    if (KIND == FK_U8 && k < int(S.n) && S.s[k].combine != FK_REDUCE_SUM && S.s[k].op == kNoOp &&
+        S.s[k].lane_kind == FK_U8) {
       const bool mx = S.s[k].combine == FK_REDUCE_MAX;
       const uint32_t m = mm2(pk[k], pk[k] >> 16, mx) & 0xffu;
       if (mx ? uint32_t(a1[k]) < m : m < uint32_t(a1[k])) acc[k].v[0] = m;

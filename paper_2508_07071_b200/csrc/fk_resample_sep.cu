@@ -53,58 +53,3 @@ cudaError_t launch_resample_sep(int src_lanes, uint32_t out_lane_kind, bool spli
 }
 
 }  // namespace fk
-
-namespace fk {
-
-uint32_t resample_tma_ring() { return kTRing; }
-size_t resample_tma_fix_bytes() { return sizeof(FixShared); }
-
-// Bulk-copy producer/consumer kernel: one CTA per (band, slice), consumer warps
-// + one producer warp; dynamic shared memory = ring + per-warp fix lists.
-cudaError_t launch_resample_tma(int src_lanes, uint32_t out_lane_kind, bool split, uint32_t sig, const DPlan& P,
-                                cudaStream_t st) {
-  if (P.width == 0 || P.height == 0 || P.batch == 0) return cudaSuccess;
-  const uint32_t spc = P.slots ? P.slots_per_cta : 1u;
-  const uint32_t slices = P.slots ? P.slices : P.batch;
-  const uint32_t nwarps = (spc * P.slot_threads + 31) / 32;
-  const dim3 grid(1, (P.height + P.tiles_per_cta - 1) / P.tiles_per_cta, slices);
-  const uint32_t block = 32 * (nwarps + 1);
-  const size_t smem = size_t(kTRing) * spc * P.ring_span + size_t(nwarps) * sizeof(FixShared);
-#define FK_RT(NL, OLK, SP, S)                                                                        \
-  do {                                                                                               \
-    auto k = fk_resample_tma<NL, OLK, SP, S>;                                                        \
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));                 \
-    k<<<grid, block, smem, st>>>(P);                                                                 \
-  } while (0)
-  if (sig != kSigLut) {
-#define FK_CASE(S)                                          \
-  if (sig == (S)) {                                         \
-    if (src_lanes == 3 && split) FK_RT(3, FK_F32, true, S); \
-    else if (src_lanes == 3) FK_RT(3, FK_F32, false, S);    \
-    else FK_RT(1, FK_F32, false, S);                        \
-    return cudaGetLastError();                              \
-  }
-    FK_AFFINE_SIGS(FK_CASE)
-#undef FK_CASE
-    return cudaErrorInvalidValue;
-  }
-  if (src_lanes == 3) {
-    if (split) {
-      if (out_lane_kind == FK_U8) FK_RT(3, FK_U8, true, kSigLut);
-      else if (out_lane_kind == FK_F32) FK_RT(3, FK_F32, true, kSigLut);
-      else FK_RT(3, FK_F64, true, kSigLut);
-    } else {
-      if (out_lane_kind == FK_U8) FK_RT(3, FK_U8, false, kSigLut);
-      else if (out_lane_kind == FK_F32) FK_RT(3, FK_F32, false, kSigLut);
-      else FK_RT(3, FK_F64, false, kSigLut);
-    }
-  } else {
-    if (out_lane_kind == FK_U8) FK_RT(1, FK_U8, false, kSigLut);
-    else if (out_lane_kind == FK_F32) FK_RT(1, FK_F32, false, kSigLut);
-    else FK_RT(1, FK_F64, false, kSigLut);
-  }
-#undef FK_RT
-  return cudaGetLastError();
-}
-
-}  // namespace fk

@@ -608,31 +608,6 @@ __device__ __forceinline__ void pair_bilinear(const DSample& s, const DWrite& w,
   }
 }
 
-// mbarrier / bulk-copy primitives (the staged walk's bulk form and the TMA walk)
-__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t tx) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(tx) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t a) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra.uni WAIT_%=;\n\t}" ::"r"(a),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_copy(uint32_t dst, uint64_t src, uint32_t bytes, uint32_t mbar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
-               "l"(src), "r"(bytes), "r"(mbar)
-               : "memory");
-}
-
 // ------------------------------------------------- staged (cp.async) walk --
 // Each visit's source row is new to the warp, so a direct tap load is an L2
 // round trip. The staged walk instead copies the row span the warp's columns
@@ -666,11 +641,6 @@ struct StagePlan {
   uint64_t g;            // copy job: source address of the chunk in relative row 0
   uint32_t pitch, dst, n;  // ... row pitch, byte offset in a ring row, bytes (0: none)
   uint32_t ta[2], tb[2];  // byte offsets of tap a / b of columns x, x + 1 in a ring row
-  // whole-span bulk copies (cp.async.bulk), warp-uniform: one per plane slot in
-  // the warp; usable when the 16-byte rounded spans stay inside the source view
-  bool bulk;
-  uint64_t bg[2];
-  uint32_t bpitch[2], bbytes[2], bdst[2];
 };
 
 template <int NL>
@@ -711,20 +681,6 @@ __device__ __forceinline__ StagePlan stage_plan(const DSample& s, bool mine, uin
   S.pitch = pit;
   S.dst = (jobA ? 0u : kRingRow / 2) * (hA == hB ? 0u : 1u) + 16 * c;
   S.n = (jobA || jobB) ? min(16u, vend - start) : 0u;
-  // bulk form: group A from lane 0's plane, group B from lane 31's
-  const uint32_t tail = s.tail_bytes;
-  const uint32_t tailA = __shfl_sync(0xffffffffu, tail, 0), tailB = __shfl_sync(0xffffffffu, tail, 31);
-  const uint64_t oA = __shfl_sync(0xffffffffu, origin, 0), oB = __shfl_sync(0xffffffffu, origin, 31);
-  const uint32_t pA = __shfl_sync(0xffffffffu, uint32_t(s.pitch), 0), pB = __shfl_sync(0xffffffffu, uint32_t(s.pitch), 31);
-  S.bulk = (nA == 0 || spA + 16 * nA <= tailA) && (nB == 0 || spB + 16 * nB <= tailB);
-  S.bg[0] = oA + spA;
-  S.bg[1] = oB + spB;
-  S.bpitch[0] = pA;
-  S.bpitch[1] = pB;
-  S.bbytes[0] = 16 * nA;
-  S.bbytes[1] = 16 * nB;
-  S.bdst[0] = 0;
-  S.bdst[1] = hA == hB ? 0u : kRingRow / 2;
   return S;
 }
 
@@ -734,14 +690,11 @@ __device__ __forceinline__ uint32_t pin(uint32_t v) {
   return v;
 }
 
-// BULK: the warp's lane 0 stages each row with one cp.async.bulk per plane slot,
-// completing on the slot's mbarrier (mbar: kRing per-warp barriers); otherwise
-// every lane copies a 16-byte chunk with cp.async (zero-filled past the crop).
-// Measured on C5: 1.87 ms bulk vs 1.63-1.71 ms cp.async (small ~400-byte bulk
-// copies + mbarrier spins), so BULK is opt-in (FK_SEP_BULK=1).
-template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool VEC, bool BULK, class Out, class KS>
+// Every lane copies a 16-byte chunk of the visit's row span with cp.async
+// (zero-filled past the crop) kRing - 1 visits ahead.
+template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool VEC, class Out, class KS>
 __device__ __forceinline__ void pair_bilinear_staged(const DWrite& w, const BandRows& R, const Visits& V,
-                                                     uint8_t* ring, uint64_t* mbar, const StagePlan& S,
+                                                     uint8_t* ring, const StagePlan& S,
                                                      const XEnt& e0, const XEnt& e1, bool active, uint32_t x,
                                                      bool col1, uint32_t y0, bool swap, bool al, const KS& ks,
                                                      const Out* lut, FixList& fix) {
@@ -762,33 +715,11 @@ __device__ __forceinline__ void pair_bilinear_staged(const DWrite& w, const Band
   Cur out(w, x, y0, swap);
   const uint32_t nv = V.n;
   const uint32_t lane = threadIdx.x & 31u;
-  const uint32_t mb = uint32_t(__cvta_generic_to_shared(mbar));
-  // bulk staging of visit j into ring slot `slot` (lane 0)
-  auto bulk_row = [&](uint32_t j_row, uint32_t slot_off, uint32_t bar) {
-    mbar_expect_tx(bar, S.bbytes[0] + S.bbytes[1]);
+  // prologue: visits 0 .. kRing - 2 in flight (one commit group per visit)
 #pragma unroll
-    for (int h = 0; h < 2; ++h)
-      if (S.bbytes[h]) bulk_copy(base + slot_off + S.bdst[h], at_row(S.bg[h], j_row, S.bpitch[h]), S.bbytes[h], bar);
-  };
-  if constexpr (BULK) {
-    if (lane == 0) {
-#pragma unroll
-      for (uint32_t j = 0; j < kRing; ++j) mbar_init(mb + 8 * j, 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    __syncwarp();
-    if (lane == 0) {
-#pragma unroll
-      for (uint32_t j = 0; j < kRing - 1; ++j)
-        if (j < nv) bulk_row(visit_row(lds32(vp + 4 * j)), j * kRingRow, mb + 8 * j);
-    }
-  } else {
-    // prologue: visits 0 .. kRing - 2 in flight (one commit group per visit)
-#pragma unroll
-    for (uint32_t j = 0; j < kRing - 1; ++j) {
-      if (j < nv && S.n) cp_async16(cdst + j * kRingRow, at_row(S.g, visit_row(lds32(vp + 4 * j)), S.pitch), S.n);
-      cp_commit();
-    }
+  for (uint32_t j = 0; j < kRing - 1; ++j) {
+    if (j < nv && S.n) cp_async16(cdst + j * kRingRow, at_row(S.g, visit_row(lds32(vp + 4 * j)), S.pitch), S.n);
+    cp_commit();
   }
   uint64_t hA[3] = {0, 0, 0}, hB[3] = {0, 0, 0};
   uint32_t k = 0;
@@ -797,18 +728,11 @@ __device__ __forceinline__ void pair_bilinear_staged(const DWrite& w, const Band
   auto visit = [&](auto U, uint32_t i, uint64_t (&cur)[3], const uint64_t (&prev)[3]) {
     constexpr uint32_t u = decltype(U)::value;
     constexpr uint32_t slot = u * kRingRow, aslot = ((u + kRing - 1) % kRing) * kRingRow;
-    if constexpr (BULK) {
-      mbar_wait(mb + 8 * u, (i / kRing) & 1u);  // visit i's row has landed
-      __syncwarp();                              // every lane is done with visit i - 1's slot
-      if (lane == 0 && i + kRing - 1 < nv)
-        bulk_row(visit_row(lds32(vp + 4 * (u + kRing - 1))), aslot, mb + 8 * ((u + kRing - 1) % kRing));
-    } else {
-      cp_wait<kRing - 2>();  // visit i's row has landed (this lane's chunk) ...
-      __syncwarp();           // ... and every lane's; every lane is also done with visit i - 1's slot
-      if (i + kRing - 1 < nv && S.n)
-        cp_async16(cdst + aslot, at_row(S.g, visit_row(lds32(vp + 4 * (u + kRing - 1))), S.pitch), S.n);
-      cp_commit();
-    }
+    cp_wait<kRing - 2>();  // visit i's row has landed (this lane's chunk) ...
+    __syncwarp();           // ... and every lane's; every lane is also done with visit i - 1's slot
+    if (i + kRing - 1 < nv && S.n)
+      cp_async16(cdst + aslot, at_row(S.g, visit_row(lds32(vp + 4 * (u + kRing - 1))), S.pitch), S.n);
+    cp_commit();
     const uint32_t ta0 = __funnelshift_r(lds32(a0 + slot), lds32(a0 + slot + 4), sa0);
     const uint32_t tb0 = __funnelshift_r(lds32(b0 + slot), lds32(b0 + slot + 4), sb0);
     const uint32_t ta1 = __funnelshift_r(lds32(a1 + slot), lds32(a1 + slot + 4), sa1);
@@ -842,7 +766,7 @@ __device__ __forceinline__ void pair_bilinear_staged(const DWrite& w, const Band
     if (i0 + 7 >= nv) break;
     visit(std::integral_constant<uint32_t, 7 % kRing>(), i0 + 7, hB, hA);
   }
-  if constexpr (!BULK) cp_wait<0>();
+  cp_wait<0>();
   __syncwarp();  // the ring and its barriers are reused by the next slice
 }
 
@@ -887,95 +811,6 @@ __device__ __forceinline__ void pair_tap(const DSample& s, const DWrite& w, cons
   }
 }
 
-// ------------------------------------------- bulk-copy (TMA) producer walk --
-// One CTA = one warp slice (consumer warps) + one producer warp. Per visit the
-// producer's elected lane issues ONE cp.async.bulk per plane slot — the whole
-// span of source bytes that slot's columns touch in that row — into a ring of
-// kTRing row buffers, completing on the slot's `full` mbarrier; consumers wait
-// on it, gather taps, lerp, emit, and release the buffer on its `empty`
-// mbarrier. No per-lane copy, commit or warp-wide wait in the consumers' walk.
-// Measured on C5 it is SLOWER than the per-warp cp.async ring (1.78 vs 1.62 ms:
-// the consumers spin on `full` — one producer lane paced by the slowest of the
-// seven consumer warps), so it is opt-in (FK_SEP_TMA=1) for A/B work.
-#ifndef FK_TRING
-#define FK_TRING 4
-#endif
-constexpr uint32_t kTRing = FK_TRING;  // staged rows (kTRing - 1 visits ahead of the slowest consumer)
-
-// The span of source bytes plane slot columns [c0, c1) touch, 16-byte aligned.
-template <int NL>
-__device__ __forceinline__ void slot_span(const DSample& s, uint32_t c0, uint32_t c1, uint32_t& lo, uint32_t& bytes) {
-  const XEnt a = dev::x_entry(s, c0, NL), b = dev::x_entry(s, c1 - 1, NL);
-  lo = a.o0 & ~15u;
-  bytes = (b.o1 + NL - lo + 15) & ~15u;
-}
-
-template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG, bool VEC, class Out, class KS>
-__device__ __forceinline__ void pair_bilinear_tma(const DWrite& w, const BandRows& R, const Visits& V, uint32_t ring,
-                                                  uint32_t bars, uint32_t slot_bytes, uint32_t span_lo,
-                                                  uint32_t region, const XEnt& e0, const XEnt& e1, bool mine,
-                                                  bool active, uint32_t x, bool col1, uint32_t y0, bool swap, bool al,
-                                                  const KS& ks, const Out* lut, FixList& fix) {
-  const uint64_t fx = f2::pack(float(e0.f), float(e1.f));
-  const float col_thr = (coord_exact8(e0.f) && coord_exact8(e1.f)) ? 0.5f : 0.5f - kNearTol;
-  const uint32_t bias = pin(bias_reg());
-  const uint32_t ta0 = mine ? region + e0.o0 - span_lo : 0u, tb0 = mine ? region + e0.o1 - span_lo : 0u;
-  const uint32_t ta1 = mine ? region + e1.o0 - span_lo : 0u, tb1 = mine ? region + e1.o1 - span_lo : 0u;
-  const uint32_t a0 = pin(ring + (ta0 & ~3u)), b0 = pin(ring + (tb0 & ~3u));
-  const uint32_t a1 = pin(ring + (ta1 & ~3u)), b1 = pin(ring + (tb1 & ~3u));
-  const uint32_t sa0 = 8 * (ta0 & 3u), sb0 = 8 * (tb0 & 3u), sa1 = 8 * (ta1 & 3u), sb1 = 8 * (tb1 & 3u);
-  uint32_t vp = pin(uint32_t(__cvta_generic_to_shared(V.v)));
-  uint32_t qp = pin(uint32_t(__cvta_generic_to_shared(R.q)));
-  using Cur = typename std::conditional<VEC, VecOut, PairOut<NL, OLK, SPLIT>>::type;
-  Cur out(w, x, y0, swap);
-  const uint32_t nv = V.n;
-  const uint32_t lane = threadIdx.x & 31u;
-  uint64_t hA[3] = {0, 0, 0}, hB[3] = {0, 0, 0};
-  uint32_t k = 0;
-  auto visit = [&](auto U, uint32_t i, uint64_t (&cur)[3], const uint64_t (&prev)[3]) {
-    constexpr uint32_t u = decltype(U)::value;
-    constexpr uint32_t soff = u * 0;  // slot offsets are runtime (slot_bytes)
-    (void)soff;
-    const uint32_t rb = u * slot_bytes;
-    mbar_wait(bars + 8 * u, (i / kTRing) & 1u);  // full[u]: visit i's row has landed
-    const uint32_t xa0 = __funnelshift_r(lds32(a0 + rb), lds32(a0 + rb + 4), sa0);
-    const uint32_t xb0 = __funnelshift_r(lds32(b0 + rb), lds32(b0 + rb + 4), sb0);
-    const uint32_t xa1 = __funnelshift_r(lds32(a1 + rb), lds32(a1 + rb + 4), sa1);
-    const uint32_t xb1 = __funnelshift_r(lds32(b1 + rb), lds32(b1 + rb + 4), sb1);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(bars + 8 * (kTRing + u));  // empty[u]: this warp is done with the buffer
-    hlerp2<NL>(xa0, xb0, xa1, xb1, fx, bias, cur);
-    const uint32_t end = visit_end(lds32(vp + 4 * u));
-    if (active) {
-#pragma unroll 1
-      for (; k < end; ++k, qp += 8) {
-        float2 q;
-        asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(q.x), "=f"(q.y) : "r"(qp));
-        emit2<NL, OLK, SPLIT, SIG, VEC, Out>(prev, cur, q, k, col_thr, ks, lut, swap, col1, al, out, fix);
-      }
-    }
-  };
-  for (uint32_t i0 = 0; i0 < nv; i0 += kTRing, vp += 4 * kTRing) {
-    static_assert(kTRing == 4 || kTRing == 8, "the walk is unrolled by the ring size");
-    visit(std::integral_constant<uint32_t, 0>(), i0, hA, hB);
-    if (i0 + 1 >= nv) break;
-    visit(std::integral_constant<uint32_t, 1>(), i0 + 1, hB, hA);
-    if (i0 + 2 >= nv) break;
-    visit(std::integral_constant<uint32_t, 2>(), i0 + 2, hA, hB);
-    if (i0 + 3 >= nv) break;
-    visit(std::integral_constant<uint32_t, 3>(), i0 + 3, hB, hA);
-    if (kTRing == 4) continue;
-    if (i0 + 4 >= nv) break;
-    visit(std::integral_constant<uint32_t, 4 % kTRing>(), i0 + 4, hA, hB);
-    if (i0 + 5 >= nv) break;
-    visit(std::integral_constant<uint32_t, 5 % kTRing>(), i0 + 5, hB, hA);
-    if (i0 + 6 >= nv) break;
-    visit(std::integral_constant<uint32_t, 6 % kTRing>(), i0 + 6, hA, hB);
-    if (i0 + 7 >= nv) break;
-    visit(std::integral_constant<uint32_t, 7 % kTRing>(), i0 + 7, hB, hA);
-  }
-}
-
 }  // namespace
 
 // One CTA = ONE warp, an independent unit of work: 32 column pairs of a band of
@@ -998,7 +833,6 @@ __global__ void __launch_bounds__(32, FK_SEP_MINB) fk_resample_sep(const __grid_
   __shared__ FixShared fixs;
   __shared__ Out lut[AFFINE ? 1 : 2 * NL * 256];
   __shared__ alignas(16) uint8_t ring[STAGED ? kRing * kRingRow : 16];
-  __shared__ alignas(8) uint64_t mbar[kRing];
   __shared__ float kscr[24];
   const uint32_t lane = threadIdx.x;
   const uint32_t T = P.slot_threads;  // column pairs per plane slot
@@ -1082,28 +916,24 @@ __global__ void __launch_bounds__(32, FK_SEP_MINB) fk_resample_sep(const __grid_
         if (!S.ok) __trap();  // the host checked spans and alignment (sep_stage_ok)
         if (__all_sync(0xffffffffu, vec || !active)) {
           // slots share their lane swap, so `swap` is warp-uniform
-          if (AFFINE && P.aff_inline && !swap && S.bulk && !P.no_bulk) {  // the configs[1]/[4] path
-            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, true, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
-                                                                       col1, y_begin, swap, al,
-                                                                       KPin<NL, SIG, false>(P, kscr), my_lut, fix);
-          } else if (AFFINE && P.aff_inline && !swap) {
-            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, false, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
+          if (AFFINE && P.aff_inline && !swap) {
+            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring, S, e0, e1, active, x,
                                                                         col1, y_begin, swap, al,
                                                                         KPin<NL, SIG, false>(P, kscr), my_lut, fix);
           } else if (AFFINE && P.aff_inline) {
-            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, false, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
+            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring, S, e0, e1, active, x,
                                                                         col1, y_begin, swap, al,
                                                                         KPin<NL, SIG, true>(P, kscr), my_lut, fix);
           } else {
             AffConsts K;
             if constexpr (AFFINE) load_affine<NL, SIG>(P, z, swap, K);
-            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, false, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
+            pair_bilinear_staged<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring, S, e0, e1, active, x,
                                                                         col1, y_begin, swap, al, KReg{K}, my_lut, fix);
           }
         } else {
           AffConsts K;
           if constexpr (AFFINE) load_affine<NL, SIG>(P, z, swap, K);
-          pair_bilinear_staged<NL, OLK, SPLIT, SIG, false, false, Out>(w, R, vis, ring, mbar, S, e0, e1, active, x,
+          pair_bilinear_staged<NL, OLK, SPLIT, SIG, false, Out>(w, R, vis, ring, S, e0, e1, active, x,
                                                                        col1, y_begin, swap, al, KReg{K}, my_lut, fix);
         }
       } else if (bilinear && active) {
@@ -1137,162 +967,6 @@ __global__ void __launch_bounds__(32, FK_SEP_MINB) fk_resample_sep(const __grid_
         for (uint32_t y = y_begin; y < y_end; ++y) fix_pair<NL, OLK, SPLIT, SIG, Out>(P, z, x, y, my_lut);
     }
   }
-}
-
-// Bulk-copy producer/consumer form of the column walk (see pair_bilinear_tma):
-// CTA = the consumer warps of one slice (P.slot_threads pairs per plane slot,
-// slots_per_cta slots) + a producer warp. Bilinear planes only; the host checks
-// 16-byte alignment, span capacity and that the rounded spans stay inside the
-// source view (DSample::tail_bytes). Dynamic shared memory: kTRing ring rows of
-// slots_per_cta * P.ring_span bytes, then the per-warp fix lists.
-template <int NL, uint32_t OLK, bool SPLIT, uint32_t SIG>
-__global__ void __launch_bounds__(256, 3) fk_resample_tma(const __grid_constant__ DPlan P) {
-  constexpr bool AFFINE = SIG != kSigLut;
-  using Out = typename std::conditional<OLK == FK_F64, uint64_t, uint32_t>::type;
-  extern __shared__ __align__(128) uint8_t dyn[];
-  __shared__ BandRows R;
-  __shared__ Visits vis;
-  __shared__ __align__(8) uint64_t bars[2 * kTRing];
-  __shared__ float kscr[24];  // every consumer warp stages the same constants
-  __shared__ Out lut[AFFINE ? 1 : 2 * NL * 256];
-  const uint32_t spc = P.slots ? P.slots_per_cta : 1u;
-  const uint32_t T = P.slot_threads;
-  const uint32_t nwarps = (spc * T + 31) / 32;  // consumer warps; warp nwarps = producer
-  const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31u;
-  const uint32_t slot_bytes = spc * P.ring_span;
-  uint8_t* ring = dyn;
-  FixShared* fixs = reinterpret_cast<FixShared*>(dyn + kTRing * slot_bytes) + (warp < nwarps ? warp : 0);
-  const uint32_t c = blockIdx.z;
-  auto plane_of = [&](uint32_t h) -> uint32_t {
-    if (h >= spc) return kNoPlane;
-    if (P.slots) return __ldg(P.slots + c * spc + h);
-    return P.order ? __ldg(P.order + c) : c;
-  };
-  const uint32_t y_begin = blockIdx.y * P.tiles_per_cta;
-  const uint32_t y_end = min(y_begin + P.tiles_per_cta, P.height);
-  const uint32_t z0 = plane_of(0);
-  const DSample s0 = P.reads[z0];
-  // row table (all threads), visit list (warp 0), barriers (thread 0)
-  for (uint32_t j = threadIdx.x; j < y_end - y_begin; j += blockDim.x) {
-    const YEnt ye = dev::y_entry(s0, y_begin + j);
-    const double f = ye.f;
-    R.q[j] = make_float2(float(f), coord_exact8(f) ? 0.5f : 0.5f - kNearTol);
-    R.s[j] = (uint32_t(ye.r0 / s0.pitch) - s0.y0) | ((uint32_t(ye.r1 / s0.pitch) - s0.y0) << 16);
-  }
-  if constexpr (!AFFINE) {
-    for (uint32_t h = 0; h < spc; ++h) {
-      const uint32_t zh = plane_of(h);
-      if (zh == kNoPlane) continue;
-      const DSample sh = P.reads[zh];
-      const bool swh = ((sh.flags & SF_POST_SWAP) != 0) != (P.prog_swap != 0);
-      for (uint32_t t = threadIdx.x; t < 256; t += blockDim.x) {
-        uint64_t v[1][3] = {{t, t, t}};
-        dev::run_ops(P, sh.post_off, sh.post_len, zh, v);
-        dev::run_ops(P, P.op_base, P.n_ops, zh, v);
-#pragma unroll
-        for (int m = 0; m < NL; ++m) lut[(h * NL + m) * 256 + t] = Out(v[0][(NL == 3 && swh) ? 2 - m : m]);
-      }
-    }
-  }
-  if (threadIdx.x == 0) {
-    const uint32_t b = uint32_t(__cvta_generic_to_shared(bars));
-    for (uint32_t i = 0; i < kTRing; ++i) {
-      mbar_init(b + 8 * i, 1);                       // full: the producer's expect_tx arrival
-      mbar_init(b + 8 * (kTRing + i), nwarps);       // empty: one arrival per consumer warp
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (warp == 0) build_visits_warp(R, y_end - y_begin, vis);
-  if (warp < nwarps && lane == 0) fixs->n = 0;
-  __syncthreads();
-  const uint32_t bars_s = uint32_t(__cvta_generic_to_shared(bars));
-  const uint32_t ring_s = uint32_t(__cvta_generic_to_shared(ring));
-  if (warp == nwarps) {  // producer: one bulk copy per plane slot per visit
-    if (lane != 0) return;
-    uint64_t org[4];
-    uint32_t pit[4], lo[4], bytes[4], tx = 0;
-    for (uint32_t h = 0; h < spc; ++h) {
-      const uint32_t zh = plane_of(h);
-      bytes[h] = 0;
-      if (zh == kNoPlane) continue;
-      const DSample sh = P.reads[zh];
-      const uint32_t c1 = min(2 * T, P.width);
-      slot_span<NL>(sh, 0, c1, lo[h], bytes[h]);
-      org[h] = sh.src + uint64_t(sh.y0) * sh.pitch + lo[h];
-      pit[h] = uint32_t(sh.pitch);
-      tx += bytes[h];
-    }
-    const uint32_t nv = vis.n;
-    for (uint32_t i = 0; i < nv; ++i) {
-      const uint32_t u = i % kTRing;
-      if (i >= kTRing) mbar_wait(bars_s + 8 * (kTRing + u), ((i / kTRing) - 1) & 1u);
-      mbar_expect_tx(bars_s + 8 * u, tx);
-      const uint32_t row = visit_row(vis.v[i]);
-      for (uint32_t h = 0; h < spc; ++h)
-        if (bytes[h]) bulk_copy(ring_s + u * slot_bytes + h * P.ring_span, at_row(org[h], row, pit[h]), bytes[h],
-                                bars_s + 8 * u);
-    }
-    return;
-  }
-  // consumers
-  const uint32_t ts = warp * 32 + lane;
-  const uint32_t hs = ts / T;
-  const uint32_t x = 2 * (ts - hs * T);
-  const uint32_t zm = plane_of(hs);
-  const bool slot_on = zm != kNoPlane;
-  const uint32_t z = slot_on ? zm : z0;
-  const DSample s = P.reads[z];
-  const DWrite w = P.writes[z];
-  const bool swap = ((s.flags & SF_POST_SWAP) != 0) != (P.prog_swap != 0);
-  const bool mine = slot_on && x < P.width;
-  const bool active = mine && (w.flags & WF_ACTIVE);
-  const bool col1 = x + 1 < P.width;
-  const bool al = (w.flags & WF_LANE_ALIGNED) != 0;
-  const Out* my_lut = lut + (AFFINE ? 0 : (hs < spc ? hs : 0) * NL * 256);
-  const XEnt e0 = dev::x_entry(s, mine ? x : 0, NL);
-  const XEnt e1 = dev::x_entry(s, mine && col1 ? x + 1 : (mine ? x : 0), NL);
-  uint32_t span_lo = 0, span_bytes = 0;
-  slot_span<NL>(s, 0, min(2 * T, P.width), span_lo, span_bytes);
-  const uint32_t region = (hs < spc ? hs : 0) * P.ring_span;
-  bool vec = false;
-  if constexpr (SPLIT && OLK == FK_F32) {
-    vec = col1 && w.pitch[1] == w.pitch[0] && w.pitch[2] == w.pitch[0];
-#pragma unroll
-    for (int d = 0; d < 3; ++d) vec = vec && ((w.dst[d] | w.pitch[d]) & 7) == 0;
-  }
-  FixList fix{fixs, false};
-  if (__all_sync(0xffffffffu, vec || !active)) {
-    if (AFFINE && P.aff_inline && !swap)
-      pair_bilinear_tma<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring_s, bars_s, slot_bytes, span_lo, region, e0, e1,
-                                                        mine, active, x, col1, y_begin, swap, al,
-                                                        KPin<NL, SIG, false>(P, kscr), my_lut, fix);
-    else if (AFFINE && P.aff_inline)
-      pair_bilinear_tma<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring_s, bars_s, slot_bytes, span_lo, region, e0, e1,
-                                                        mine, active, x, col1, y_begin, swap, al,
-                                                        KPin<NL, SIG, true>(P, kscr), my_lut, fix);
-    else {
-      AffConsts K;
-      if constexpr (AFFINE) load_affine<NL, SIG>(P, z, swap, K);
-      pair_bilinear_tma<NL, OLK, SPLIT, SIG, true, Out>(w, R, vis, ring_s, bars_s, slot_bytes, span_lo, region, e0, e1,
-                                                        mine, active, x, col1, y_begin, swap, al, KReg{K}, my_lut, fix);
-    }
-  } else {
-    AffConsts K;
-    if constexpr (AFFINE) load_affine<NL, SIG>(P, z, swap, K);
-    pair_bilinear_tma<NL, OLK, SPLIT, SIG, false, Out>(w, R, vis, ring_s, bars_s, slot_bytes, span_lo, region, e0, e1,
-                                                       mine, active, x, col1, y_begin, swap, al, KReg{K}, my_lut, fix);
-  }
-  // the filter's flagged pixels of this warp, exactly
-  __syncwarp();
-  const uint32_t n = min(fixs->n, kFixCap);
-  for (uint32_t i = lane; i < n; i += 32) {
-    const uint32_t ent = fixs->e[i], y = y_begin + (ent >> 5);
-    const uint32_t tse = warp * 32 + (ent & 31u), he = tse / T, ze = plane_of(he);
-    fix_pair<NL, OLK, SPLIT, SIG, Out>(P, ze, 2 * (tse - he * T), y, lut + (AFFINE ? 0 : he * NL * 256));
-  }
-  if (fix.ovf)
-    for (uint32_t y = y_begin; y < y_end; ++y) fix_pair<NL, OLK, SPLIT, SIG, Out>(P, z, x, y, my_lut);
 }
 
 }  // namespace fk

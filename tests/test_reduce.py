@@ -213,3 +213,35 @@ def test_cuda_plain_rows(oracle, dt, kind):
         kinds = [kind, kind, kind, kind, cast_to]
         for x, y, (c, _, _), k in zip(res[0][0], res[1][0], specs_of(oracle), kinds):
             close(x, y, c, k)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("kind", [U8, U8X3])
+def test_cuda_plain_rows_mixed_value_kinds(oracle, kind):
+    """Plain u8 rows folded by u8-valued Max/Min specs (packed 16x2 lanes) next
+    to f32-valued Max/Min specs (cast transforms) in the same traversal, on data
+    whose extrema are non-zero (10..255): the packed lanes must only join the
+    specs that fed them (an f32 Min returned 0.0 instead of 10.0)."""
+    cuda = Library("cuda")
+    rng = np.random.default_rng(5)
+    shape = (300, 1024, 3) if kind == U8X3 else (300, 1024)
+    big = rng.integers(10, 256, shape, dtype=np.uint8)
+    to = F32X3 if kind == U8X3 else F32
+    n = 3 if kind == U8X3 else 1
+    spec_sets = [
+        lambda lib: [(REDUCE_MIN, lib.op_cast(kind, to), None), (REDUCE_MIN, None, None),
+                     (REDUCE_MAX, lib.op_cast(kind, to), None), (REDUCE_MAX, None, None)],
+        lambda lib: [(REDUCE_MIN, lib.op_cast(kind, to), of.const_of(to, *([300.0] * n))),
+                     (REDUCE_MIN, None, of.const_of(kind, *([200] * n))),
+                     (REDUCE_SUM, None, None), (REDUCE_MAX, lib.op_cast(kind, to), None)],
+    ]
+    for specs_of in spec_sets:
+        res = []
+        for lib in (cuda, oracle):
+            p = lib.plane_from_numpy(big, kind)
+            res.append(lib.multi_reduce_plane(lib.op_read_per_thread(p), specs_of(lib)))
+        assert cuda.last_kernel().startswith("fk_reduce_plain"), cuda.last_kernel()
+        for x, y, (c, t, _) in zip(res[0][0], res[1][0], specs_of(oracle)):
+            close(x, y, c, kind if t is None else to)
+        mins = [v for (c, t, _), v in zip(specs_of(oracle), res[0][0]) if c == REDUCE_MIN]
+        assert all(min(v) >= 10 for v in mins), mins
