@@ -115,6 +115,7 @@ struct DPlan {
   uint32_t no_stage;         // 1: column-streaming kernel uses direct tap loads (spans the ring cannot hold)
   uint32_t dir_rep[4];       // fk_direct: repeat count of chain op k (its constant / reciprocal in aff_c / aff_r [k][0])
   FastDiv zdiv;              // fk_reduce: n / tiles (plane of a linear tile index)
+  uint64_t negz;             // (-0.0f, -0.0f) at run time: packed products as fma(a, b, negz) (fk_pack2.cuh)
 };
 constexpr uint32_t kNoPlane = 0xffffffffu;
 

@@ -72,9 +72,11 @@ __device__ __forceinline__ void up(uint64_t v, float& lo, float& hi) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
 }
 template <uint32_t FN>
-__device__ __forceinline__ uint64_t op(uint64_t a, uint64_t b) {
+__device__ __forceinline__ uint64_t op(uint64_t a, uint64_t b, uint64_t z) {
   uint64_t d;
-  if constexpr (FN == AF_MUL) asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  // a product as fma(a, b, z), z the runtime -0 pair: ptxas contracts a packed
+  // mul + add into FFMA2 even with .rn (fk_pack2.cuh)
+  if constexpr (FN == AF_MUL) asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(z));
   else if constexpr (FN == AF_ADD) asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   else asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
   return d;
@@ -82,7 +84,7 @@ __device__ __forceinline__ uint64_t op(uint64_t a, uint64_t b) {
 }  // namespace p2
 
 template <uint32_t SIG, int K>
-__device__ __forceinline__ void direct_op(float (&v)[kD], float c, float r, uint32_t reps) {
+__device__ __forceinline__ void direct_op(float (&v)[kD], float c, float r, uint32_t reps, uint64_t z) {
   if constexpr (K < sig_n(SIG) && sig_fn(SIG, K) != AF_DIV && FK_DIRECT_FP2) {
     // Mul / Add / Sub: packed pairs
     constexpr uint32_t FN = sig_fn(SIG, K);
@@ -93,7 +95,7 @@ __device__ __forceinline__ void direct_op(float (&v)[kD], float c, float r, uint
 #pragma unroll 1
     for (uint32_t i = 0; i < reps; ++i)
 #pragma unroll
-      for (int e = 0; e < kD / 2; ++e) q[e] = p2::op<FN>(q[e], cc);
+      for (int e = 0; e < kD / 2; ++e) q[e] = p2::op<FN>(q[e], cc, z);
 #pragma unroll
     for (int e = 0; e < kD / 2; ++e) p2::up(q[e], v[2 * e], v[2 * e + 1]);
   } else if constexpr (K < sig_n(SIG)) {
@@ -194,10 +196,10 @@ template <uint32_t SIG, bool TO_U8>
 __device__ __forceinline__ void finish_tile(const DPlan& P, const DWrite& w, TileAt at, uint32_t lane, float (&v)[kD],
                                             const float (&c)[4], const float (&r)[4], const uint32_t (&rep)[4]) {
   const bool st = (w.flags & WF_STREAM) != 0;
-  direct_op<SIG, 0>(v, c[0], r[0], rep[0]);
-  direct_op<SIG, 1>(v, c[1], r[1], rep[1]);
-  direct_op<SIG, 2>(v, c[2], r[2], rep[2]);
-  direct_op<SIG, 3>(v, c[3], r[3], rep[3]);
+  direct_op<SIG, 0>(v, c[0], r[0], rep[0], P.negz);
+  direct_op<SIG, 1>(v, c[1], r[1], rep[1], P.negz);
+  direct_op<SIG, 2>(v, c[2], r[2], rep[2], P.negz);
+  direct_op<SIG, 3>(v, c[3], r[3], rep[3], P.negz);
   uint8_t* row = reinterpret_cast<uint8_t*>(w.dst[0]) + uint64_t(at.y) * w.pitch[0];
   const uint32_t ob = TO_U8 ? 1u : 4u;
   if (at.x0 + kWarpTile <= P.width && ((reinterpret_cast<uintptr_t>(row) + uint64_t(at.x0) * ob) & (4 * ob - 1)) == 0) {

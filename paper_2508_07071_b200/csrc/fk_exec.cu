@@ -20,7 +20,8 @@
 #include <tuple>
 
 #include "fk_core.hpp"
-#include "fk_crop.hpp"
+#include "fk_pack2.cuh"
+#include "fk_walk.hpp"
 #include "fk_reduce.hpp"
 #include "fk_exec.hpp"
 #include "fk_launch.hpp"
@@ -198,11 +199,11 @@ struct DeviceProgram {
   uint64_t def[3] = {0, 0, 0};
   uint32_t def_kind = 0;
   Traffic traffic;               // analytic ExecReport counters (computed once)
-  // planar crop kernel (fk_crop.cu): crop -> bilinear -> [swap] -> f32 chain -> split f32
-  bool crop_ok = false;
-  bool crop_perz = false;        // per-plane chain constants (BatchArith or per-plane lane swaps)
-  uint32_t crop_sig = 0;
-  CropPlan crop{};               // tables, order, inline constants (reads / writes set at launch)
+  // column-walk crop kernel (fk_walk.cu): crop -> bilinear -> [swap] -> f32 chain -> split f32
+  bool walk_ok = false;
+  bool walk_perz = false;        // per-plane chain constants (BatchArith or per-plane lane swaps)
+  uint32_t walk_sig = 0;
+  WalkPlan walk{};               // units, tables, inline constants (reads set at launch)
 
   ~DeviceProgram() {
     for (void* p : {static_cast<void*>(d_table), static_cast<void*>(d_reads), static_cast<void*>(d_writes),
@@ -293,47 +294,47 @@ void keep_pool_memory(int device) {
 // floor(a / b) for b > 0
 int64_t floor_div(int64_t a, int64_t b) { return a >= 0 ? a / b : -((-a + b - 1) / b); }
 
-// CropRow for output row y (fk_crop.hpp): center_coord / floor / clamp of
-// ops.cpp:253-275 in exact integers, and the dp2a weights of the vertical lerp.
-CropRow crop_row(uint32_t y, uint32_t rect_h, uint32_t out_h) {
+// WalkRow for output row y (fk_walk.hpp): center_coord / floor / clamp of
+// ops.cpp:253-275 in exact integers: cy = P / den, P = (2y + 1) rect_h - out_h,
+// den = 2 out_h, iy = floor(P / den), fy = (P - iy den) / den.
+WalkRow walk_row(uint32_t y, uint32_t rect_h, uint32_t out_h) {
   const int64_t den = 2 * int64_t(out_h);
   const int64_t P = (2 * int64_t(y) + 1) * rect_h - out_h;
   const int64_t iy = floor_div(P, den), ny = P - iy * den;
   const int64_t maxy = int64_t(rect_h) - 1;
   const uint32_t iy0 = uint32_t(std::min(std::max<int64_t>(iy, 0), maxy));
   const uint32_t iy1 = uint32_t(std::min(std::max<int64_t>(iy + 1, 0), maxy));
-  CropRow r{};
-  uint32_t K, d, n;
-  const bool exact = (ny * 64) % den == 0;  // fy a multiple of 1/64: den 64, K 256, every FP32 step exact
-  if (exact) {
-    d = 64; n = uint32_t(ny * 64 / den); K = 256;
-  } else {
-    d = uint32_t(den); n = uint32_t(ny); K = uint32_t(8388607 / (255 * den));  // K d 255 < 2^23
-  }
-  r.iy = iy0 | (iy1 << 16) | (exact ? kCropExact : 0u);
-  r.wts = (K * (d - n)) | ((K * n) << 16);
-  r.s = float(64.0 / (double(K) * d));
-  r.c = -131072.0f * r.s;  // exact: a power-of-two multiple
+  WalkRow r{};
+  const bool same = iy0 == iy1;
+  r.r1 = iy1 | (same ? kWalkSame : 0u) | ((same || (ny * 128) % den == 0) ? kWalkExactRow : 0u);
+  r.fy = same ? 0.0f : float(double(ny) / double(den));
   return r;
 }
 
-// CropCol for output column x: left tap (relative, clamped) and the reference's
-// fx (cx - floor(cx) in double, ops.cpp:262-266) rounded to f32; 0 where both
-// taps clamp to one column.
-CropCol crop_col(uint32_t x, uint32_t rect_w, uint32_t out_w) {
+// WalkCol for output column x: the left tap (clamped) and the dp2a weights /
+// pixel scale of the horizontal lerp (fk_walk.hpp).
+WalkCol walk_col(uint32_t x, uint32_t rect_w, uint32_t out_w) {
   const int64_t den = 2 * int64_t(out_w);
   const int64_t P = (2 * int64_t(x) + 1) * rect_w - out_w;
   const int64_t ix = floor_div(P, den), nx = P - ix * den;
   const int64_t maxx = int64_t(rect_w) - 1;
-  CropCol c{};
-  if (ix < 0 || ix + 1 > maxx) {
-    c.ix = uint32_t(ix < 0 ? 0 : maxx) | kCropExact;
-    c.fx = 0.0f;
-    return c;
+  const uint32_t ix0 = uint32_t(std::min(std::max<int64_t>(ix, 0), maxx));
+  const uint32_t ix1 = uint32_t(std::min(std::max<int64_t>(ix + 1, 0), maxx));
+  WalkCol c{};
+  c.tap = 3 * ix0;
+  if (ix0 == ix1 || (nx * 128) % den == 0) {  // exact: units of 2^-14 pixel
+    const uint32_t j = ix0 == ix1 ? 0u : uint32_t(nx * 16384 / den);
+    c.wts = (16384u - j) | (j << 16);
+    c.s = 1.0f / 16384.0f;
+    c.c = -512.0f;
+    c.thr = 0.5f;
+  } else {
+    const uint32_t K = uint32_t(8388607 / (255 * den));
+    c.wts = uint32_t(K * (den - nx)) | (uint32_t(K * nx) << 16);
+    c.s = float(1.0 / double(K * den));
+    c.c = float(-8388608.0 / double(K * den));
+    c.thr = kWalkThr;
   }
-  const double cx = (double(x) + 0.5) * double(rect_w) / double(out_w) - 0.5;
-  c.ix = uint32_t(ix) | ((nx * 256) % den == 0 ? kCropExact : 0u);
-  c.fx = float(cx - std::floor(cx));
   return c;
 }
 
@@ -372,24 +373,28 @@ bool recip2_div_exact(const std::vector<DOp>& arith, size_t k, const std::map<ui
   return true;
 }
 
-// Eligibility, tables and constants of the planar crop kernel: every plane a
-// bilinear crop of a u8x3 frame (4-byte aligned rows), an AFFINE chain, a
-// split write of three f32 planes with one 16-byte multiple pitch.
-void build_crop(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& arith, uint32_t sig,
+// Eligibility, tables, units, TMA tensor maps and constants of the
+// column-walk crop kernel (fk_walk.cu): every plane a bilinear crop (or a crop
+// of the output size) of a u8x3 frame with 16-byte aligned rows, an AFFINE
+// chain, a split write of three f32 planes sharing one 8-byte multiple pitch,
+// an even output width.
+void build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& arith, uint32_t sig,
                 const std::vector<DWrite>& writes) {
   const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
   const uint32_t wid = p.write.id == FK_OP_BATCH_WRITE ? p.write.w_inner : p.write.id;
-  if (!dp.affine_ok || dp.resample_lanes != 3 || wid != FK_OP_SPLIT_WRITE || B == 0 || W % 4 || W / 4 > kCropMaxQuads ||
-      W == 0 || H == 0 || H > 16448 || lane_kind(uint32_t(p.write.in_kind)) != FK_F32)
+  if (!dp.affine_ok || dp.resample_lanes != 3 || wid != FK_OP_SPLIT_WRITE || B == 0 || W % 2 || W == 0 || H == 0 ||
+      W > 65534 || H > 65535 || lane_kind(uint32_t(p.write.in_kind)) != FK_F32)
     return;
   bool ok = true;
-  for (const DSample& s : dp.reads)
-    ok = ok && s.mode == RD_BILINEAR && s.kind == FK_U8X3 && !(s.flags & SF_DEFAULT) && s.rect_h < 32768 &&
-         s.rect_w < (1u << 30) && ((s.src | s.pitch) & 15) == 0 && s.pitch < (1ull << 32) && s.out_w == W &&
-         s.out_h == H;
+  for (const DSample& s : dp.reads) {
+    // a crop without resize (rect == out, resizing() false) is the bilinear walk with fx = fy = 0
+    ok = ok && (s.mode == RD_BILINEAR || (s.mode == RD_DIRECT && s.rect_w == W && s.rect_h == H)) &&
+         s.kind == FK_U8X3 && !(s.flags & SF_DEFAULT) && s.rect_h <= 65535 && s.rect_w <= 65535 &&
+         ((s.src | s.pitch) & 15) == 0 && s.pitch < (1ull << 39) && s.out_w == W && s.out_h == H;
+  }
   for (const DWrite& w : writes)
     ok = ok && (w.flags & WF_ACTIVE) && w.pitch[0] == w.pitch[1] && w.pitch[0] == w.pitch[2] &&
-         (w.pitch[0] & 15) == 0 && w.pitch[0] < (1ull << 32) && ((w.dst[0] | w.dst[1] | w.dst[2]) & 15) == 0;
+         (w.pitch[0] & 7) == 0 && w.pitch[0] < (1ull << 32) && ((w.dst[0] | w.dst[1] | w.dst[2]) & 7) == 0;
   if (!ok) return;
   // chain: the AFFINE signature with the verified division forms
   uint32_t fn[4] = {0, 0, 0, 0}, fast = 0, two = 0;
@@ -399,62 +404,117 @@ void build_crop(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
     if (recip2_div_exact(arith, k, dp.per_z_host, B)) two |= 1u << k;
     else if (sig_fast(sig, int(k))) fast |= 1u << k;
   }
-  uint32_t csig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast) | (two << kCropDiv2);
-  if (!crop_registered(csig)) csig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast);
-  if (!crop_registered(csig)) csig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], 0);
-  if (!crop_registered(csig)) return;
-  // row bands: enough CTAs for ~2 waves of 4 per SM on small batches
-  const uint64_t target = 148ull * 4 * 2;
-  uint32_t bands = B >= target ? 1u
-                               : uint32_t(std::min<uint64_t>((target + B - 1) / B, (H + kCropTileRows - 1) / kCropTileRows));
-  uint32_t band_rows = (H + bands - 1) / bands;
-  band_rows = (band_rows + kCropTileRows - 1) / kCropTileRows * kCropTileRows;
-  bands = (H + band_rows - 1) / band_rows;
-  // tables: one per distinct crop height / width (out extents are uniform)
-  std::vector<CropRow> rows;
-  std::vector<CropCol> cols;
+  uint32_t wsig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast) | (two << kWalkDiv2);
+  if (!walk_registered(wsig)) wsig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast);
+  if (!walk_registered(wsig)) wsig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], 0);
+  if (!walk_registered(wsig)) return;
+
+  // tables: one per distinct crop height / width (the out extents are uniform)
+  std::vector<WalkRow> rows;
+  std::vector<WalkCol> cols;
   std::map<uint32_t, uint32_t> row_at, col_at;
-  std::vector<CropAux> aux(B);
-  uint32_t max_words = 0, max_stage = 0;
+  std::vector<WalkAux> aux(B);
+  std::vector<bool> swaps(B);
   bool swap0 = false, swap_uniform = true;
   for (uint32_t z = 0; z < B; ++z) {
     const DSample& s = dp.reads[z];
     auto r = row_at.find(s.rect_h);
     if (r == row_at.end()) {
       r = row_at.emplace(s.rect_h, uint32_t(rows.size())).first;
-      for (uint32_t y = 0; y < H; ++y) rows.push_back(crop_row(y, s.rect_h, H));
-      // source rows a tile stages: [iy0 of its first row, iy1 of its last]
-      for (uint32_t b = 0; b < bands; ++b)
-        for (uint32_t ty = b * band_rows; ty < std::min(H, (b + 1) * band_rows); ty += kCropTileRows) {
-          const uint32_t ly = std::min({H, (b + 1) * band_rows, ty + kCropTileRows}) - 1;
-          const uint32_t lo = rows[r->second + ty].iy & 0x7fffu, hi = (rows[r->second + ly].iy >> 16) & 0x7fffu;
-          max_stage = std::max(max_stage, hi - lo + 1);
-        }
+      for (uint32_t y = 0; y < H; ++y) rows.push_back(walk_row(y, s.rect_h, H));
+      rows.push_back(WalkRow{kWalkRowMask, 0.0f});  // sentinel: the walk reads one row ahead
     }
     auto c = col_at.find(s.rect_w);
     if (c == col_at.end()) {
       c = col_at.emplace(s.rect_w, uint32_t(cols.size())).first;
-      for (uint32_t x = 0; x < W; ++x) cols.push_back(crop_col(x, s.rect_w, W));
+      for (uint32_t x = 0; x < W; ++x) cols.push_back(walk_col(x, s.rect_w, W));
     }
-    CropAux& a = aux[z];
-    a.rowtab = r->second;
+    WalkAux& a = aux[z];
+    const bool swap = ((s.flags & SF_POST_SWAP) != 0) != dp.fused_swap;
+    if (z == 0) swap0 = swap;
+    swap_uniform = swap_uniform && swap == swap0;
+    swaps[z] = swap;
+    for (int m = 0; m < 3; ++m) a.dst[m] = writes[z].dst[swap ? 2 - m : m];
+    a.dpitch = uint32_t(writes[z].pitch[0]);
+    a.x3 = 3 * s.x0;
     a.coltab = c->second;
-    const uint32_t first = s.x0 + (cols[c->second].ix & ~kCropExact);
-    const uint32_t last = s.x0 + (cols[c->second + W - 1].ix & ~kCropExact) + 1;  // + the right tap
-    a.wb = (3 * first) & ~15u;
-    a.nwords = ((3 * (last + 1) - a.wb + 15) / 16) * 4;
-    // the crop's last row may be the frame's last: staging zero-fills past its readable bytes
-    // (every real byte, < 3 (x0 + rect_w), is readable)
-    if (uint64_t(3) * (s.x0 + s.rect_w) > s.tail_bytes) return;
-    a.rlim = s.tail_bytes > a.wb ? s.tail_bytes - a.wb : 0u;
-    a.swap = (((s.flags & SF_POST_SWAP) != 0) != dp.fused_swap) ? 1u : 0u;
-    if (z == 0) swap0 = a.swap;
-    swap_uniform = swap_uniform && a.swap == uint32_t(swap0);
     a.kz = z;
-    max_words = std::max(max_words, a.nwords);
   }
-  const uint32_t v_stride = max_words * 16, stage_stride = max_words * 4;
-  if (crop_smem_bytes(v_stride, max_stage, stage_stride, W / 4) > 200 * 1024) return;
+  // units: two half strips of 32 output columns (16 lanes, 2 columns each) per
+  // warp, paired among the halves of planes with the same crop height
+  struct Half { uint32_t z, x, n; };
+  std::map<uint32_t, std::vector<Half>> by_h;  // rect_h -> half strips, plane order
+  for (uint32_t z = 0; z < B; ++z)
+    for (uint32_t x = 0; x < W; x += 2 * kWalkHalfLanes)
+      by_h[dp.reads[z].rect_h].push_back(Half{z, x, std::min(kWalkHalfLanes, (W - x) / 2)});
+  const uint64_t halves = uint64_t(B) * ((W + 2 * kWalkHalfLanes - 1) / (2 * kWalkHalfLanes));
+  const uint64_t target = 148ull * 28 * 3;  // three waves of 28 warps per SM
+  uint32_t bands = uint32_t(std::min<uint64_t>((2 * target + halves - 1) / halves, (H + 7) / 8));
+  bands = std::max({bands, 1u, (H + kWalkMaxRows - 1) / kWalkMaxRows});
+  const uint32_t band_rows = (H + bands - 1) / bands;
+  bands = (H + band_rows - 1) / band_rows;
+  std::vector<WalkUnit> units;
+  uint32_t row_bytes = 16;
+  // one half: plane z, columns [x, x + 2n): the staged span [2 bx, ...) of each crop row
+  auto half = [&](WalkUnit& u, int h, const Half& hf) {
+    const DSample& s = dp.reads[hf.z];
+    const WalkCol* ct = &cols[aux[hf.z].coltab];
+    const uint32_t first = 3 * s.x0 + ct[hf.x].tap, last = 3 * s.x0 + ct[hf.x + 2 * hf.n - 1].tap;
+    const uint32_t wb = first & ~15u;
+    row_bytes = std::max(row_bytes, (last + 6 - wb + 15) & ~15u);
+    u.z[h] = hf.z;
+    u.bx[h] = uint16_t(wb / 2);
+    u.x[h] = uint16_t(hf.x);
+    u.n[h] = uint16_t(hf.n);
+    ok = ok && wb / 2 < 65536;
+  };
+  for (uint32_t b = 0; b < bands; ++b) {
+    const uint32_t y_lo = b * band_rows, y_hi = std::min(H, y_lo + band_rows);
+    for (auto& kv : by_h) {
+      const WalkRow* rt = &rows[row_at[kv.first]];
+      const std::vector<Half>& hs = kv.second;
+      for (size_t i = 0; i < hs.size(); i += 2) {
+        WalkUnit u{};
+        const bool two = i + 1 < hs.size();
+        half(u, 0, hs[i]);
+        half(u, 1, two ? hs[i + 1] : hs[i]);
+        if (!two) u.n[1] = 0;
+        u.y_lo = uint16_t(y_lo);
+        u.y_hi = uint16_t(y_hi);
+        const uint32_t r1 = rt[y_lo].r1 & kWalkRowMask;
+        u.r_first = uint16_t((rt[y_lo].r1 & kWalkSame) ? r1 : r1 - 1);
+        u.r_last = uint16_t(rt[y_hi - 1].r1 & kWalkRowMask);
+        u.rowtab = row_at[kv.first];
+        units.push_back(u);
+      }
+    }
+  }
+  // TMA tensor maps: per plane, its crop's rows [y0, y0 + rect_h) as elements
+  // of 2, 4 or 8 bytes (the smallest whose 256-element box holds a staged row)
+  // over [0, ceil(3 (x0 + rect_w) / elem)): the last element of a row may
+  // extend past the crop, so that byte range must be readable in its last row
+  row_bytes = (row_bytes + 31) & ~31u;  // 4-row boxes stay 128-byte aligned in shared memory
+  const uint32_t elem = row_bytes <= 512 ? 2 : row_bytes <= 1024 ? 4 : 8;
+  if (!ok || units.empty() || row_bytes > 256 * elem) return;
+  if (walk_smem_bytes(row_bytes, band_rows) > 200 * 1024) return;
+  std::vector<CUtensorMap> maps(B);
+  for (uint32_t z = 0; z < B && ok; ++z) {
+    const DSample& s = dp.reads[z];
+    const uint64_t end = 3ull * (s.x0 + s.rect_w), width = (end + elem - 1) / elem;
+    ok = width * elem <= s.tail_bytes &&
+         walk_encode_map(&maps[z], s.src + uint64_t(s.y0) * s.pitch, width, s.rect_h, s.pitch, elem,
+                         row_bytes / elem, kWalkGroup);
+  }
+  for (WalkUnit& u : units)
+    for (int h = 0; h < 2; ++h) u.bx[h] = uint16_t(u.bx[h] * 2 / elem);  // bx was in 2-byte elements
+  if (!ok) return;
+  // units of one source frame back to back (the frame stays L2-resident while
+  // its crops run), longest first within a frame (walk cost ~ visits + rows)
+  std::stable_sort(units.begin(), units.end(), [&](const WalkUnit& a, const WalkUnit& b) {
+    const uint64_t sa = dp.reads[a.z[0]].src, sb = dp.reads[b.z[0]].src;
+    if (sa != sb) return sa < sb;
+    return 2u * (a.r_last - a.r_first) + 5u * (a.y_hi - a.y_lo) > 2u * (b.r_last - b.r_first) + 5u * (b.y_hi - b.y_lo);
+  });
   bool perz = !swap_uniform;
   for (const DOp& d : arith) perz = perz || d.per_z;
   // constants, input-lane order: lane m of plane z uses output lane sigma_z(m)
@@ -471,15 +531,15 @@ void build_crop(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
     h = 1.0f / c;
     l = (two >> k) & 1u ? float(1.0 / double(c) - double(h)) : -c;
   };
-  CropPlan& P = dp.crop;
-  P = CropPlan{};
+  WalkPlan& P = dp.walk;
+  P = WalkPlan{};
   if (perz) {
     std::vector<float4> kz(size_t(B) * 12, make_float4(0, 0, 0, 0));
     for (uint32_t z = 0; z < B; ++z)
       for (size_t k = 0; k < arith.size(); ++k)
         for (int m = 0; m < 3; ++m) {
           float c, h, l;
-          consts(k, z, m, aux[z].swap != 0, c, h, l);
+          consts(k, z, m, swaps[z], c, h, l);
           kz[size_t(z) * 12 + 3 * k + m] = make_float4(c, h, l, 0.0f);
         }
     P.kz = upload(kz);
@@ -494,33 +554,23 @@ void build_crop(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
         P.kl[k][m] = make_float2(l, l);
       }
   }
-  // visiting order: crops of one source frame back to back (the frame stays
-  // L2-resident while its crops run), widest spans first within a frame
-  std::vector<uint32_t> order(B);
-  for (uint32_t z = 0; z < B; ++z) order[z] = z;
-  std::stable_sort(order.begin(), order.end(), [&](uint32_t a, uint32_t b) {
-    if (dp.reads[a].src != dp.reads[b].src) return dp.reads[a].src < dp.reads[b].src;
-    return aux[a].nwords > aux[b].nwords;
-  });
+  P.units = upload(units);
   P.aux = upload(aux);
   P.rows = upload(rows);
   P.cols = upload(cols);
-  P.order = upload(order);
-  for (const void* q : {static_cast<const void*>(P.aux), static_cast<const void*>(P.rows),
-                        static_cast<const void*>(P.cols), static_cast<const void*>(P.order)})
+  P.maps = upload(maps);
+  for (const void* q : {static_cast<const void*>(P.units), static_cast<const void*>(P.aux),
+                        static_cast<const void*>(P.rows), static_cast<const void*>(P.cols),
+                        static_cast<const void*>(P.maps)})
     dp.extra.push_back(const_cast<void*>(q));
-  P.out_w = W;
-  P.out_h = H;
-  P.quads = W / 4;
-  P.v_stride = v_stride;
-  P.stage_rows = max_stage;
-  P.stage_stride = stage_stride;
-  P.n_planes = B;
-  P.bands = bands;
-  P.band_rows = band_rows;
-  dp.crop_ok = true;
-  dp.crop_perz = perz;
-  dp.crop_sig = csig;
+  P.n_units = uint32_t(units.size());
+  P.row_bytes = row_bytes;
+  P.elem = elem;
+  P.negz = kNegZero2;
+  P.max_rows = band_rows;
+  dp.walk_ok = true;
+  dp.walk_perz = perz;
+  dp.walk_sig = wsig;
 }
 
 bool sep_stage_ok(const DeviceProgram& dp, uint32_t W, uint32_t T, uint32_t spc);
@@ -722,7 +772,7 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
         }
       }
     }
-    build_crop(*dp, p, arith, sig, writes);
+    build_walk(*dp, p, arith, sig, writes);
   }
   // direct f32 kernel: f32 planes read as-is, f32 arith runs (any repeat), an
   // optional final Cast f32 -> u8, a packed write
@@ -818,6 +868,7 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
 
 DPlan base_plan(uint32_t W, uint32_t H, uint32_t B, bool flat, int E) {
   DPlan P{};
+  P.negz = kNegZero2;
   if (flat) {
     W = W * H;
     H = 1;
@@ -1014,13 +1065,12 @@ fk_exec_report execute_fused(const Pipeline& p, const fk_exec_config* cfg) {
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     r.path = FK_PATH_COMPILED;
-  } else if (affine && dp.crop_ok) {
-    // planar crop kernel: one CTA per (plane, row band), vertical-first two-phase tiles
-    CropPlan C = dp.crop;
+  } else if (affine && dp.walk_ok) {
+    // column-walk crop kernel: one warp per (64-column strip, row band), source rows visited once
+    WalkPlan C = dp.walk;
     C.reads = dp.d_reads;
-    C.writes = dp.d_writes;
-    cuda_check(launch_crop(dp.crop_sig, dp.crop_perz, C, C.n_planes * C.bands, st), "fk_crop launch");
-    t_last_kernel = "fk_crop";
+    cuda_check(launch_walk(dp.walk_sig, dp.walk_perz, C, st), "fk_walk launch");
+    t_last_kernel = "fk_walk";
     ++r.kernels_launched;
     g_launches.fetch_add(1, std::memory_order_relaxed);
     r.path = FK_PATH_COMPILED;

@@ -91,7 +91,8 @@ __device__ __forceinline__ uint64_t fma(uint64_t a, uint64_t b, uint64_t c) {
 template <uint32_t SIG, int K>
 __device__ __forceinline__ uint64_t sig_op2(uint64_t v, float c, float r) {
   constexpr uint32_t fn = sig_fn(SIG, K);
-  if constexpr (fn == AF_MUL) return f2::mul(v, f2::bc(c));
+  // a chain product as two scalar mul.rn: ptxas contracts a packed mul + add into FFMA2 (fk_pack2.cuh)
+  if constexpr (fn == AF_MUL) return f2::pack(__fmul_rn(f2::lo(v), c), __fmul_rn(f2::hi(v), c));
   else if constexpr (fn == AF_ADD) return f2::add(v, f2::bc(c));
   else if constexpr (fn == AF_SUB) return f2::sub(v, f2::bc(c));
   else if constexpr (sig_fast(SIG, K)) {  // div_by_recip: q = x r; e = fma(-q, d, x); q + e r

@@ -1,0 +1,493 @@
+// fk_walk.cu — the column-walk crop kernel: a batch of crops of u8x3 frames,
+// bilinear-resized (ops.cpp:259-299), [SwapRB], cast to f32, an f32 chain
+// (sub mean / div std, ...) and split into three f32 planes, ONE fused launch
+// (configs[1], [3], [4]; horizontal fusion: the batch index z is a warp's unit).
+//
+// Structure. Every warp is independent (no CTA barrier): it owns two half
+// strips of 32 output columns (two per lane) — of one plane, or of two planes
+// with the same crop height, so a 224-wide plane is 3.5 warps without idle
+// lanes — and a band of output rows. Bilinear is separable; the warp walks the
+// source rows the band needs, top to bottom, each visited ONCE:
+//
+//   stage   lane 0 copies 4 source rows of each half's byte span at a time
+//           into a per-warp shared-memory ring, one 2D TMA tensor copy per
+//           half (cp.async.bulk.tensor, the crop's rows as a tensor map; rows
+//           and bytes outside the crop read as zeros), completion on an
+//           mbarrier, 4-8 rows ahead (no LSU traffic, no registers);
+//   H       each lane lerps row r horizontally at its two columns as exact
+//           integers: three 32-bit shared loads, a funnel shift to the
+//           column's byte offset, two byte_perm and three dp2a per column
+//           (see WalkCol: H lands in the mantissa of 2^23);
+//   finish  every output row whose lower source row is r: vertical lerp of the
+//           two H rows in packed FP32 (FFMA2 over the lane's column pair), the
+//           exact-result filter, cast + chain in packed FP32, and one 8-byte
+//           streaming store per destination plane (a warp writes 256
+//           contiguous bytes per plane).
+//
+// Exact-result filter. v (FP32, pixel units) differs from the exact rational
+// bilinear value R by at most 6.2e-5 on non-exact columns/rows (dp2a exact; the
+// FFMA2 vertical lerp <= 0.75 units of 1 / (K den); s and c rounded; the final
+// rounding; bound derived in DESIGN.md §4), and the reference's double result
+// differs from R by < 1e-12. So when |v - rint(v)| <= 0.5 - E (E = 2^-13) the
+// reference's nearbyint(res) is rint(v). Values outside the band are recomputed
+// by their lane in the reference's double arithmetic, op for op, and stored
+// over the fast value (same thread, program order). Where the column AND row
+// fractions are dyadic with <= 7 bits every FP32 step is exact (v == R), so the
+// check is off there (threshold 0.5) and exact ties round to even like the
+// reference's nearbyint.
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include "fk_pack2.cuh"
+#include "fk_walk.hpp"
+#include "fk_stages.cuh"
+#include "fk_sig.cuh"
+
+#ifndef FK_WALK_MINB
+#define FK_WALK_MINB 6  // CTAs of 4 warps per SM (80 registers: no spills)
+#endif
+
+namespace fk {
+
+namespace {
+
+
+constexpr float kRound = 12582912.0f;        // 1.5 * 2^23: x + kRound rounds x to an integer (ties to even)
+
+// The chain's constants for input lane m, op k, as pairs: c, and for a division
+// either (r_hi, r_lo) [two-op form] or (RN(1/c), -c) [three-op form].
+struct KInl {
+  const WalkPlan& P;
+  uint64_t z;  // runtime -0 pair (fk_pack2.cuh)
+  __device__ __forceinline__ uint64_t c(int k, int m) const { return p2::of(P.kc[k][m]); }
+  __device__ __forceinline__ uint64_t h(int k, int m) const { return p2::of(P.kh[k][m]); }
+  __device__ __forceinline__ uint64_t l(int k, int m) const { return p2::of(P.kl[k][m]); }
+};
+template <uint32_t SIG>
+struct KReg {
+  uint64_t cc[4][3], hh[4][3], ll[4][3];
+  uint64_t z;  // runtime -0 pair (fk_pack2.cuh)
+  __device__ __forceinline__ KReg(const float4* kz, uint64_t negz) : z(negz) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        if (k < sig_n(SIG)) {
+          const float4 v = __ldg(kz + 3 * k + m);
+          cc[k][m] = p2::pack(v.x, v.x);
+          hh[k][m] = p2::pack(v.y, v.y);
+          ll[k][m] = p2::pack(v.z, v.z);
+        } else {
+          cc[k][m] = hh[k][m] = ll[k][m] = 0;
+        }
+      }
+  }
+  __device__ __forceinline__ uint64_t c(int k, int m) const { return cc[k][m]; }
+  __device__ __forceinline__ uint64_t h(int k, int m) const { return hh[k][m]; }
+  __device__ __forceinline__ uint64_t l(int k, int m) const { return ll[k][m]; }
+};
+
+__host__ __device__ constexpr bool div2(uint32_t sig, int k) { return (sig >> (kWalkDiv2 + k)) & 1u; }
+
+// The registered chain on a column pair: the reference's arith ops
+// (ops.cpp:88-159), same IEEE ops in the same order; divisions in a
+// host-verified form.
+template <uint32_t SIG, int K, class KS>
+__device__ __forceinline__ uint64_t chain_op2(uint64_t x, const KS& ks, int m) {
+  constexpr uint32_t fn = sig_fn(SIG, K);
+  if constexpr (fn == AF_MUL) return p2::mul_z(x, ks.c(K, m), ks.z);
+  else if constexpr (fn == AF_ADD) return p2::add(x, ks.c(K, m));
+  else if constexpr (fn == AF_SUB) return p2::sub(x, ks.c(K, m));
+  else if constexpr (div2(SIG, K)) return p2::fma(x, ks.h(K, m), p2::mul(x, ks.l(K, m)));
+  else if constexpr (sig_fast(SIG, K)) {  // q = x r; e = fma(q, -c, x) [l holds -c]; q + e r
+    const uint64_t q = p2::mul(x, ks.h(K, m));
+    const uint64_t e = p2::fma(q, ks.l(K, m), x);
+    return p2::fma(e, ks.h(K, m), q);
+  } else {
+    const float c = p2::lo(ks.c(K, m));
+    return p2::pack(__fdiv_rn(p2::lo(x), c), __fdiv_rn(p2::hi(x), c));
+  }
+}
+template <uint32_t SIG, class KS>
+__device__ __forceinline__ uint64_t chain2(uint64_t x, const KS& ks, int m) {
+  if constexpr (sig_n(SIG) > 0) x = chain_op2<SIG, 0>(x, ks, m);
+  if constexpr (sig_n(SIG) > 1) x = chain_op2<SIG, 1>(x, ks, m);
+  if constexpr (sig_n(SIG) > 2) x = chain_op2<SIG, 2>(x, ks, m);
+  if constexpr (sig_n(SIG) > 3) x = chain_op2<SIG, 3>(x, ks, m);
+  return x;
+}
+
+// ------------------------------------------------------------- fix path --
+// The reference's bilinear value of one lane in double, op for op
+// (ops.cpp:250,283-296), rounded like round_clamp_u8 (nearbyint; the value is
+// in [0, 255]), as the float of the u8 result.
+__device__ __forceinline__ float exact_lane(uint32_t a, uint32_t b, uint32_t c, uint32_t d, double fx, double fy) {
+  const double top = __dadd_rn(double(a), __dmul_rn(__dsub_rn(double(b), double(a)), fx));
+  const double bot = __dadd_rn(double(c), __dmul_rn(__dsub_rn(double(d), double(c)), fx));
+  const double res = __dadd_rn(top, __dmul_rn(__dsub_rn(bot, top), fy));
+  return float(uint32_t(__double2loint(__dadd_rn(res, 6755399441055744.0))) & 0xffu);
+}
+
+// Both columns (x, x + 1) and the three lanes of output row y of plane z,
+// recomputed exactly as the reference does (bilinear_sample in double,
+// round_clamp_u8, the chain in IEEE f32 op by op) and stored over the fast
+// values. Runs for lanes whose fast value came within E of a rounding boundary.
+template <uint32_t SIG, bool PERZ>
+__device__ __noinline__ void fix_pair(const WalkPlan& P, uint32_t z, uint32_t x, uint32_t y) {
+  const DSample s = P.reads[z];
+  const WalkAux A = P.aux[z];
+  const float4* kz = PERZ ? P.kz + 12ull * A.kz : nullptr;
+  const YEnt ye = dev::y_entry(s, y);
+  const uint8_t* r0 = reinterpret_cast<const uint8_t*>(s.src) + ye.r0;
+  const uint8_t* r1 = reinterpret_cast<const uint8_t*>(s.src) + ye.r1;
+  for (uint32_t c = 0; c < 2; ++c) {
+    const XEnt xe = dev::x_entry(s, x + c, 3);
+    for (int m = 0; m < 3; ++m) {
+      float v = exact_lane(__ldg(r0 + xe.o0 + m), __ldg(r0 + xe.o1 + m), __ldg(r1 + xe.o0 + m), __ldg(r1 + xe.o1 + m),
+                           xe.f, ye.f);
+#pragma unroll
+      for (int k = 0; k < sig_n(SIG); ++k) {
+        const float cst = PERZ ? __ldg(kz + 3 * k + m).x : P.kc[k][m].x;
+        switch (sig_fn(SIG, k)) {
+          case AF_MUL: v = __fmul_rn(v, cst); break;
+          case AF_ADD: v = __fadd_rn(v, cst); break;
+          case AF_SUB: v = __fsub_rn(v, cst); break;
+          default: v = __fdiv_rn(v, cst); break;
+        }
+      }
+      __stcs(reinterpret_cast<float*>(A.dst[m] + uint64_t(y) * A.dpitch) + x + c, v);
+    }
+  }
+}
+
+// The flagged values of output row y of lane `owner` of warp unit u (its
+// plane and columns recomputed from the unit, as fk_walk assigns them).
+template <uint32_t SIG, bool PERZ>
+__device__ __forceinline__ void fix_owner(const WalkPlan& P, uint32_t u, uint32_t owner, uint32_t y) {
+  const WalkUnit& U = P.units[u];
+  const uint32_t n0 = U.n[0];
+  const bool h = owner >= n0;
+  const uint32_t x = (h ? U.x[1] : U.x[0]) + 2u * (h ? owner - n0 : owner);
+  fix_pair<SIG, PERZ>(P, h ? U.z[1] : U.z[0], x, y);
+}
+
+// ------------------------------------------------------- TMA tensor copies --
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t a, uint32_t tx) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(tx) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra.uni WAIT_%=;\n\t}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+// kWalkGroup source rows of one crop (box at element (x, row y)) into shared memory
+__device__ __forceinline__ void tma_rows(uint32_t dst, uint64_t map, uint32_t x, uint32_t y, uint32_t mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(dst), "l"(map), "r"(x), "r"(y), "r"(mbar)
+      : "memory");
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ WalkRow ld_row(const WalkRow* p) {
+  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
+  return WalkRow{v.x, __uint_as_float(v.y)};
+}
+// base + a * b in one IMAD.WIDE (the compiler would share a * b across the three planes)
+__device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t base) {
+  uint64_t d;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(base));
+  return d;
+}
+__device__ __forceinline__ void st_cs2(uint64_t addr, uint64_t v) {
+  asm volatile("st.global.cs.b64 [%0], %1;" ::"l"(addr), "l"(v) : "memory");
+}
+
+// H of one visited source row at the lane's two columns: three exact integers
+// (lanes R, G, B) per column as biased floats 2^23 + H.
+__device__ __forceinline__ void h_row(uint32_t base, const uint32_t (&w)[2], const uint32_t (&sh)[2],
+                                      const uint32_t (&wts)[2], float (&H)[2][3]) {
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const uint32_t a = base + w[c];
+    const uint32_t w0 = lds32(a), w1 = lds32(a + 4), w2 = lds32(a + 8);
+    const uint32_t lo = __funnelshift_r(w0, w1, sh[c]), hi = __funnelshift_r(w1, w2, sh[c]);
+    const uint32_t rg = __byte_perm(lo, hi, 0x4130);  // (a_R, b_R, a_G, b_G)
+    const uint32_t b = __byte_perm(lo, hi, 0x0052);   // (a_B, b_B, -, -)
+    H[c][0] = __uint_as_float(__dp2a_lo(wts[c], rg, kWalkBias));
+    H[c][1] = __uint_as_float(__dp2a_hi(wts[c], rg, kWalkBias));
+    H[c][2] = __uint_as_float(__dp2a_lo(wts[c], b, kWalkBias));
+  }
+}
+
+// Per-warp shared memory: the ring (kWalkSlots slots x 2 halves x kWalkGroup
+// rows), the slots' mbarriers, lane 0's staging arguments, the fix masks (one
+// lane mask per output row of the unit), slack for the last row's 12-byte
+// window; 128-byte aligned (TMA destinations).
+struct StageArgs {
+  uint64_t map0, map1;  // tensor maps of the two halves' planes
+  uint32_t bx0, bx1;    // box x of each half
+  uint32_t two;         // half 1 present
+  uint32_t pad;
+};
+__host__ __device__ constexpr uint32_t walk_ring_bytes(uint32_t rb) { return kWalkSlots * 2 * kWalkGroup * rb; }
+__host__ __device__ constexpr uint32_t walk_warp_bytes(uint32_t rb, uint32_t max_rows) {
+  return (walk_ring_bytes(rb) + 8 * kWalkSlots + uint32_t(sizeof(StageArgs)) + 4 * max_rows + 16 + 127) / 128 * 128;
+}
+
+// ------------------------------------------------------------------ kernel --
+template <uint32_t SIG, bool PERZ>
+__global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_walk(const __grid_constant__ WalkPlan P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const uint32_t wi = threadIdx.x >> 5, lane = threadIdx.x & 31u;
+  const uint32_t u = blockIdx.x * kWalkWarps + wi;
+  if (u >= P.n_units) return;  // the whole warp: no CTA-wide synchronisation follows
+  const WalkUnit U = P.units[u];
+  const uint32_t RB = P.row_bytes, HB = kWalkGroup * RB, GB = 2 * HB;
+  unsigned char* wbase = smem + wi * walk_warp_bytes(RB, P.max_rows);
+  const uint32_t ring = uint32_t(__cvta_generic_to_shared(wbase));
+  const uint32_t bar = ring + kWalkSlots * GB;
+  StageArgs* sa = reinterpret_cast<StageArgs*>(wbase + kWalkSlots * GB + 8 * kWalkSlots);
+  uint32_t* fixm = reinterpret_cast<uint32_t*>(sa + 1);
+
+  // lane role: half h, plane z, output columns x, x + 1 (fields picked with
+  // selects: a dynamic index into U would put it in local memory)
+  const uint32_t n0 = U.n[0];
+  const bool h = lane >= n0;
+  const bool active = lane < n0 + U.n[1];
+  const uint32_t z = h ? U.z[1] : U.z[0];
+  const uint32_t xh = h ? U.x[1] : U.x[0];
+  const uint32_t x = xh + 2u * (h ? lane - n0 : lane);
+  const WalkAux A = P.aux[z];
+  // column constants (inactive lanes duplicate a valid column; they never store)
+  uint32_t w[2], sh[2], wts[2];
+  float s[2], c[2], tc[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const WalkCol C = P.cols[A.coltab + (active ? x + k : xh)];
+    const uint32_t rel = A.x3 + C.tap - P.elem * (h ? U.bx[1] : U.bx[0]);
+    w[k] = (rel & ~3u) + (h ? HB : 0u);
+    sh[k] = (rel & 3u) * 8u;
+    wts[k] = C.wts;
+    s[k] = C.s;
+    c[k] = C.c;
+    tc[k] = C.thr;
+  }
+  const uint64_t s2 = p2::pack(s[0], s[1]), c2 = p2::pack(c[0], c[1]);
+  const uint64_t kR = p2::pack(kRound, kRound);
+  uint64_t dst[3];
+#pragma unroll
+  for (int m = 0; m < 3; ++m) dst[m] = A.dst[m] + 4ull * x;
+  const uint32_t dpitch = A.dpitch;
+  using KS = typename std::conditional<PERZ, KReg<SIG>, KInl>::type;
+  const KS ks = [&]() {
+    if constexpr (PERZ) return KReg<SIG>(P.kz + 12ull * A.kz, P.negz);
+    else return KInl{P, P.negz};
+  }();
+
+  // lane 0 stages group g (source rows r_first + 4 g ...) into ring slot g % 2,
+  // both halves on that slot's mbarrier; its arguments wait in shared memory
+  const uint32_t r_first = U.r_first;
+  const uint32_t nvis = uint32_t(U.r_last) - r_first + 1u, ngroups = (nvis + kWalkGroup - 1) / kWalkGroup;
+  if (lane == 0) {
+    StageArgs t;
+    t.map0 = reinterpret_cast<uint64_t>(P.maps + U.z[0]);
+    t.map1 = reinterpret_cast<uint64_t>(P.maps + U.z[1]);
+    t.bx0 = U.bx[0];
+    t.bx1 = U.bx[1];
+    t.two = U.n[1] != 0;
+    *sa = t;
+  }
+  auto stage = [&](uint32_t g) {
+    const StageArgs t = *sa;
+    const uint32_t slot = g % kWalkSlots, r = r_first + g * kWalkGroup;
+    mbar_expect_tx(bar + 8 * slot, t.two ? GB : HB);
+    tma_rows(ring + slot * GB, t.map0, t.bx0, r, bar + 8 * slot);
+    if (t.two) tma_rows(ring + slot * GB + HB, t.map1, t.bx1, r, bar + 8 * slot);
+  };
+  if (lane == 0) {
+#pragma unroll
+    for (uint32_t i = 0; i < kWalkSlots; ++i) mbar_init(bar + 8 * i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (uint32_t g = 0; g < kWalkSlots && g < ngroups; ++g) stage(g);
+  }
+  __syncwarp();
+  const uint32_t y_hi = U.y_hi, y_lo = U.y_lo;
+  uint32_t y = y_lo;
+  const WalkRow* rp = P.rows + U.rowtab + y;  // row table, walked with y
+  WalkRow R = ld_row(rp);
+  for (uint32_t i = lane; i < y_hi - y_lo; i += 32) fixm[i] = 0;
+  bool any_fix = false;  // warp-uniform
+
+  // finish output row y from the H rows of its two source rows
+  auto finish = [&](const float (&Ha)[2][3], const float (&Hb)[2][3]) {
+    const uint64_t fy2 = p2::pack(R.fy, R.fy);
+    const bool exact_row = R.r1 & kWalkExactRow;
+    const float t0 = exact_row ? tc[0] : kWalkThr, t1 = exact_row ? tc[1] : kWalkThr;
+    bool flag = false;
+#pragma unroll
+    for (int m = 0; m < 3; ++m) {
+      const uint64_t a2 = p2::pack(Ha[0][m], Ha[1][m]), b2 = p2::pack(Hb[0][m], Hb[1][m]);
+      const uint64_t p = p2::fma(p2::sub(b2, a2), fy2, a2);  // 2^23 + the vertical lerp (units of H)
+      const uint64_t v = p2::fma(p, s2, c2);                  // pixel units
+      const uint64_t k = p2::sub(p2::add(v, kR), kR);         // rint(v): the u8 result, as f32
+      const uint64_t e = p2::sub(v, k);
+      flag = flag || fabsf(p2::lo(e)) > t0 || fabsf(p2::hi(e)) > t1;
+      const uint64_t o = chain2<SIG>(k, ks, m);
+      if (active) st_cs2(mad_wide(y, dpitch, dst[m]), o);
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, flag && active);
+    if (bal) {  // rare: note the row's flagged lanes
+      if (lane == 0) fixm[y - y_lo] = bal;
+      any_fix = true;
+    }
+  };
+
+  float HA[2][3], HB2[2][3];
+  // visit k (row staged at `row`): H into Hn, then every output row it completes
+  auto visit = [&](uint32_t k, uint32_t row, float (&Hn)[2][3], float (&Hp)[2][3]) {
+    h_row(row, w, sh, wts, Hn);
+    if (k == 0) {
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+#pragma unroll
+        for (int m = 0; m < 3; ++m) Hp[i][m] = Hn[i][m];
+    }
+    const uint32_t r = r_first + k;
+    while (y < y_hi && (R.r1 & kWalkRowMask) == r) {
+      if (R.r1 & kWalkSame) finish(Hn, Hn);
+      else finish(Hp, Hn);
+      ++y;
+      R = ld_row(++rp);  // the table has a sentinel row past out_h
+    }
+  };
+  for (uint32_t g = 0; g < ngroups; ++g) {
+    const uint32_t slot = g % kWalkSlots;
+    mbar_wait(bar + 8 * slot, (g / kWalkSlots) & 1u);
+#pragma unroll 1
+    for (uint32_t q = 0; q < kWalkGroup; q += 4) {
+      const uint32_t k = g * kWalkGroup + q, row = ring + slot * GB + q * RB;
+      if (k >= nvis) break;
+      visit(k, row, HA, HB2);
+      if (k + 1 < nvis) visit(k + 1, row + RB, HB2, HA);
+      if (k + 2 < nvis) visit(k + 2, row + 2 * RB, HA, HB2);
+      if (k + 3 < nvis) visit(k + 3, row + 3 * RB, HB2, HA);
+    }
+    __syncwarp();  // every lane is done with the slot
+    if (lane == 0 && g + kWalkSlots < ngroups) stage(g + kWalkSlots);
+  }
+  // values near a rounding boundary (rare), recomputed in the reference's
+  // arithmetic: the flagged (row, lane) pairs are dealt to the warp's lanes,
+  // 32 at a time, so the double-precision path runs with full warps
+  if (any_fix) {
+    __syncwarp();  // the fast values and the masks are stored
+    uint32_t pend = 0, my_row = 0, my_owner = 0;
+    for (uint32_t i0 = 0; i0 < y_hi - y_lo; i0 += 32) {
+      const uint32_t mi = i0 + lane < y_hi - y_lo ? fixm[i0 + lane] : 0u;
+      uint32_t rows_set = __ballot_sync(0xffffffffu, mi != 0);
+      while (rows_set) {
+        const uint32_t j = __ffs(rows_set) - 1;
+        rows_set &= rows_set - 1;
+        uint32_t mask = __shfl_sync(0xffffffffu, mi, j);
+        while (mask) {
+          const uint32_t take = min(uint32_t(__popc(mask)), 32u - pend);
+          if (lane >= pend && lane < pend + take) {
+            my_row = i0 + j;
+            my_owner = __fns(mask, 0, int(lane - pend) + 1);
+          }
+          for (uint32_t t = 0; t < take; ++t) mask &= mask - 1;
+          pend += take;
+          if (pend == 32) {
+            fix_owner<SIG, PERZ>(P, u, my_owner, y_lo + my_row);
+            pend = 0;
+          }
+        }
+      }
+    }
+    if (lane < pend) fix_owner<SIG, PERZ>(P, u, my_owner, y_lo + my_row);
+  }
+}
+
+}  // namespace
+
+// Registered chains: the AFFINE signatures of fk_sig.cuh, with the two-op
+// division variants of the normalising ones.
+#define FK_WALK_SIGS(X)                                                              \
+  X(sig_make(0))                                                                     \
+  X(sig_make(1, AF_MUL)) X(sig_make(1, AF_ADD)) X(sig_make(1, AF_SUB))              \
+  X(sig_make(1, AF_DIV)) X(sig_make(1, AF_DIV, 0, 0, 0, 1))                        \
+  X(sig_make(1, AF_DIV) | (1u << kWalkDiv2))                                         \
+  X(sig_make(2, AF_SUB, AF_DIV)) X(sig_make(2, AF_SUB, AF_DIV, 0, 0, 2))            \
+  X(sig_make(2, AF_SUB, AF_DIV) | (2u << kWalkDiv2))                                 \
+  X(sig_make(2, AF_MUL, AF_ADD)) X(sig_make(2, AF_SUB, AF_MUL))                     \
+  X(sig_make(3, AF_MUL, AF_SUB, AF_DIV)) X(sig_make(3, AF_MUL, AF_SUB, AF_DIV, 0, 4)) \
+  X(sig_make(3, AF_MUL, AF_SUB, AF_DIV) | (4u << kWalkDiv2))
+
+bool walk_registered(uint32_t sig) {
+#define FK_CASE(S) if (sig == (S)) return true;
+  FK_WALK_SIGS(FK_CASE)
+#undef FK_CASE
+  return false;
+}
+
+size_t walk_smem_bytes(uint32_t row_bytes, uint32_t max_rows) {
+  return size_t(kWalkWarps) * walk_warp_bytes(row_bytes, max_rows);
+}
+
+cudaError_t launch_walk(uint32_t sig, bool per_plane, const WalkPlan& P, cudaStream_t st) {
+  if (P.n_units == 0) return cudaSuccess;
+  const size_t smem = walk_smem_bytes(P.row_bytes, P.max_rows);
+  const uint32_t ctas = (P.n_units + kWalkWarps - 1) / kWalkWarps;
+#define FK_RUN(S, PZ)                                                                  \
+  do {                                                                                 \
+    auto k = fk_walk<S, PZ>;                                                           \
+    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));   \
+    k<<<ctas, kWalkWarps * 32, smem, st>>>(P);                                         \
+  } while (0)
+#define FK_CASE(S)                        \
+  if (sig == (S)) {                       \
+    if (per_plane) FK_RUN(S, true);       \
+    else FK_RUN(S, false);                \
+    return cudaGetLastError();            \
+  }
+  FK_WALK_SIGS(FK_CASE)
+#undef FK_CASE
+#undef FK_RUN
+  return cudaErrorInvalidValue;
+}
+
+bool walk_encode_map(CUtensorMap* map, uint64_t base, uint64_t width_elems, uint64_t rows, uint64_t pitch,
+                     uint32_t elem, uint32_t box_w, uint32_t box_h) {
+  static const PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    cudaGetLastError();
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  }();
+  if (!encode) return false;
+  const cuuint64_t dims[2] = {width_elems, rows};
+  const cuuint64_t strides[1] = {pitch};
+  const cuuint32_t box[2] = {box_w, box_h};
+  const cuuint32_t es[2] = {1, 1};
+  const CUtensorMapDataType type = elem == 2   ? CU_TENSOR_MAP_DATA_TYPE_UINT16
+                                   : elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_UINT32
+                                               : CU_TENSOR_MAP_DATA_TYPE_UINT64;
+  return encode(map, type, 2, reinterpret_cast<void*>(base), dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace fk

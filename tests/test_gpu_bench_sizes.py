@@ -46,31 +46,31 @@ def run_both(build, cuda, oracle):
 def test_c5_all_8192_crops(cuda, oracle):
     rep, w = run_both(lambda lib: wl.crops_224(lib, 8192, per_crop_norm=False, name="C5"), cuda, oracle)
     assert rep.kernels_launched == 1
-    assert cuda.last_kernel() == "fk_crop", cuda.last_kernel()
+    assert cuda.last_kernel() == "fk_walk", cuda.last_kernel()
 
 
 def test_c5_shards_match_whole(cuda, oracle):
     """The bench's strong-scaling shards (first = rank * 8192 / G) are the same
     crops as the whole batch: shard 3 of 4 equals the oracle too."""
     rep, w = run_both(lambda lib: wl.crops_224(lib, 2048, per_crop_norm=False, name="C5", first=6144), cuda, oracle)
-    assert cuda.last_kernel() == "fk_crop"
+    assert cuda.last_kernel() == "fk_walk"
 
 
 def test_c4_1024_crops_per_crop_normalize(cuda, oracle):
     rep, w = run_both(lambda lib: wl.crops_224(lib, 1024, per_crop_norm=True, name="C4"), cuda, oracle)
-    assert cuda.last_kernel() == "fk_crop"
+    assert cuda.last_kernel() == "fk_walk"
 
 
 @pytest.mark.parametrize("b", [1, 2, 16, 128])
 def test_c4_small_batches_row_bands(cuda, oracle, b):
     """Small batches split each plane into row bands (more CTAs than planes)."""
     run_both(lambda lib: wl.crops_224(lib, b, per_crop_norm=True, name="C4"), cuda, oracle)
-    assert cuda.last_kernel() == "fk_crop"
+    assert cuda.last_kernel() == "fk_walk"
 
 
 def test_c2_cvgs_50_crops(cuda, oracle):
     run_both(wl.c2, cuda, oracle)
-    assert cuda.last_kernel() == "fk_crop"
+    assert cuda.last_kernel() == "fk_walk"
 
 
 def test_c1_4k(cuda, oracle):
