@@ -130,6 +130,13 @@ int32_t fk_errc_name(int32_t status, char* buf, size_t cap); /* errc_name, scala
 /* ---- planes ------------------------------------------------------------- */
 fk_status fk_plane_view(const fk_plane* p, uint32_t x0, uint32_t y0, uint32_t w, uint32_t h,
                         fk_plane* out);                          /* Plane::view, plane.cpp:91-101 */
+/* Plane::alloc, plane.cpp:60-71 (zero-initialised; row_stride 0 = width). The
+ * buffer is SHARED the way the reference's shared_ptr<TensorBuffer> is
+ * (plane.hpp:56-60,97): every IOp and pipeline built from the plane or a view
+ * of it keeps it alive, and fk_plane_free only drops the caller's reference.
+ * CUDA backend: device memory on the current device; CPU backends: host memory. */
+fk_status fk_plane_alloc(uint32_t width, uint32_t height, uint32_t kind, uint32_t row_stride, fk_plane* out);
+void fk_plane_free(fk_plane* p);
 uint32_t fk_bytes_per_element(uint32_t kind);                    /* scalar.hpp:27-37 */
 
 /* ---- IOp builders (oplib.hpp:31-76) -------------------------------------- */
@@ -175,6 +182,23 @@ fk_status fk_plan_memory_savings(const fk_pipeline* p, uint64_t* bytes);        
 /* schedule(), executor.hpp:25: writes up to `cap` (z, y_begin, y_end) triples; *count = total tasks */
 fk_status fk_schedule(const fk_extent3* space, const fk_exec_config* cfg, uint32_t* tasks,
                       uint64_t cap, uint64_t* count);
+
+/* ---- multi-GPU batch sharding ----------------------------
+ * The reference partitions a batch z-major into independent tasks
+ * (executor.cpp:52-61, ops.cpp:369-378); across GPUs each device runs the
+ * pipeline of its own contiguous z-shard. fk_execute_sharded enqueues
+ * pipelines[i] on devices[i] (cfgs[i].stream; cfgs may be NULL) for every i
+ * before waiting on any: no collective, no host sync unless FK_EXEC_TIMED is
+ * set in a cfg (then all devices are timed with events and waited for).
+ * reports may be NULL. CPU backends run the shards one after another. */
+fk_status fk_execute_sharded(const fk_pipeline* const* pipelines, const int32_t* devices, uint32_t n,
+                             const fk_exec_config* cfgs, fk_exec_report* reports);
+/* The optional final gather (reported separately from the fused step): copies
+ * bytes[i] from srcs[i] (on src_devices[i]) to dst + dst_offsets[i] on
+ * dst_device over NVLink peer copies (cudaMemcpyPeerAsync on `stream`, a stream
+ * of dst_device; NULL = legacy default). CPU backends: memcpy. */
+fk_status fk_gather(void* dst, int32_t dst_device, const uint64_t* dst_offsets, const void* const* srcs,
+                    const int32_t* src_devices, const uint64_t* bytes, uint32_t n, void* stream);
 
 /* ---- ReduceDPP (dpp.hpp:32-53, dpp.cpp:46-246) ----------------------------- */
 enum fk_reducer { FK_REDUCE_SUM = 0, FK_REDUCE_MAX = 1, FK_REDUCE_MIN = 2 }; /* Reducer, dpp.hpp:32 */

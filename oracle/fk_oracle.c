@@ -250,6 +250,28 @@ fk_status fk_plane_view(const fk_plane* p, uint32_t x0, uint32_t y0, uint32_t w,
   return FK_OK;
 }
 
+fk_status fk_plane_alloc(uint32_t width, uint32_t height, uint32_t kind, uint32_t row_stride, fk_plane* out) {
+  /* Plane::alloc, plane.cpp:60-71: host memory, zero-initialised. The oracle is
+     test infrastructure: the caller keeps the buffer alive until fk_plane_free. */
+  if (!out || !kind_ok(kind)) return fail(FK_E_INVALID_ARGUMENT, -1, "InvalidArgument: bad plane arguments");
+  uint32_t rs = row_stride ? row_stride : width;
+  if (width == 0 || height == 0 || rs < width) return fail(FK_E_CAPACITY_OVERFLOW, -1, "CapacityOverflow: extents");
+  void* p = calloc((size_t)rs * height, fk_bytes_per_element(kind));
+  if (!p) return fail(FK_E_CAPACITY_OVERFLOW, -1, "CapacityOverflow: host allocation failed");
+  out->data = p;
+  out->width = width;
+  out->height = height;
+  out->row_stride = rs;
+  out->kind = kind;
+  return FK_OK;
+}
+void fk_plane_free(fk_plane* p) {
+  if (p && p->data) {
+    free(p->data);
+    p->data = NULL;
+  }
+}
+
 static int sample_resizing(const sample_t* s) { return s->out_w != s->rect_w || s->out_h != s->rect_h; }
 static uint32_t sample_out_kind(const sample_t* s) { /* ops.hpp:88-90 */
   return s->n_post ? s->post[s->n_post - 1].out : s->source.kind;
@@ -902,6 +924,25 @@ fk_status fk_schedule(const fk_extent3* sp, const fk_exec_config* cfg, uint32_t*
 }
 
 /* execute_fused, executor.cpp:63-85: one sweep, every point read -> compute* -> write. */
+fk_status fk_execute_sharded(const fk_pipeline* const* pipelines, const int32_t* devices, uint32_t n,
+                             const fk_exec_config* cfgs, fk_exec_report* reports) {
+  /* CPU backend: the shards one after another (devices are ignored) */
+  if (n && (!pipelines || !devices)) return fail(FK_E_INVALID_ARGUMENT, -1, "InvalidArgument: null argument");
+  for (uint32_t i = 0; i < n; ++i) {
+    fk_status s = fk_execute_fused(pipelines[i], cfgs ? &cfgs[i] : NULL, reports ? &reports[i] : NULL);
+    if (s != FK_OK) return s;
+  }
+  return FK_OK;
+}
+
+fk_status fk_gather(void* dst, int32_t dst_device, const uint64_t* dst_offsets, const void* const* srcs,
+                    const int32_t* src_devices, const uint64_t* bytes, uint32_t n, void* stream) {
+  (void)dst_device; (void)src_devices; (void)stream;
+  if (n && (!dst || !dst_offsets || !srcs || !bytes)) return fail(FK_E_INVALID_ARGUMENT, -1, "InvalidArgument: null argument");
+  for (uint32_t i = 0; i < n; ++i) memcpy((uint8_t*)dst + dst_offsets[i], srcs[i], bytes[i]);
+  return FK_OK;
+}
+
 fk_status fk_execute_fused(const fk_pipeline* p, const fk_exec_config* cfg, fk_exec_report* rep) {
   if (!p) return fail(FK_E_INVALID_ARGUMENT, -1, "null pipeline");
   fk_status st = check_config(cfg);

@@ -14,6 +14,7 @@
 // copied out after it, outside the reference's own timed region
 // (ExecReport::wall_time_ns, executor.cpp:73-82), which is what gets reported.
 
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -184,6 +185,24 @@ fk_status fk_plane_view(const fk_plane* p, uint32_t x0, uint32_t y0, uint32_t w,
   return FK_OK;
 }
 
+fk_status fk_plane_alloc(uint32_t width, uint32_t height, uint32_t kind, uint32_t row_stride, fk_plane* out) {
+  // Plane::alloc, plane.cpp:60-71 (host memory; test infrastructure: freed by fk_plane_free)
+  if (!out || kind > FK_F64X3) return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: bad plane arguments");
+  const uint32_t rs = row_stride ? row_stride : width;
+  if (width == 0 || height == 0 || rs < width)
+    return set_error(1 + int32_t(Errc::CapacityOverflow), "CapacityOverflow: extents");
+  void* p = std::calloc(size_t(rs) * height, fk_bytes_per_element(kind));
+  if (!p) return set_error(1 + int32_t(Errc::CapacityOverflow), "CapacityOverflow: host allocation failed");
+  *out = fk_plane{p, width, height, rs, kind};
+  return FK_OK;
+}
+void fk_plane_free(fk_plane* p) {
+  if (p && p->data) {
+    std::free(p->data);
+    p->data = nullptr;
+  }
+}
+
 fk_status fk_op_arith(uint32_t op_id, uint32_t kind, const void* value, fk_iop** out) {
   if (op_id < FK_OP_MUL || op_id > FK_OP_DIV || kind > FK_F64X3 || !value)
     return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: bad arith op");
@@ -351,6 +370,24 @@ fk_status fk_execute_fused(const fk_pipeline* p, const fk_exec_config* c, fk_exe
   } catch (const Error& e) {
     return set_error(e);
   }
+}
+
+fk_status fk_execute_sharded(const fk_pipeline* const* pipelines, const int32_t* devices, uint32_t n,
+                             const fk_exec_config* cfgs, fk_exec_report* reports) {
+  // CPU backend: the shards one after another (devices are ignored)
+  if (n && (!pipelines || !devices)) return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: null argument");
+  for (uint32_t i = 0; i < n; ++i) {
+    const fk_status s = fk_execute_fused(pipelines[i], cfgs ? &cfgs[i] : nullptr, reports ? &reports[i] : nullptr);
+    if (s != FK_OK) return s;
+  }
+  return FK_OK;
+}
+
+fk_status fk_gather(void* dst, int32_t, const uint64_t* dst_offsets, const void* const* srcs, const int32_t*,
+                    const uint64_t* bytes, uint32_t n, void*) {
+  if (n && (!dst || !dst_offsets || !srcs || !bytes)) return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: null argument");
+  for (uint32_t i = 0; i < n; ++i) std::memcpy(static_cast<uint8_t*>(dst) + dst_offsets[i], srcs[i], bytes[i]);
+  return FK_OK;
 }
 
 fk_status fk_execute_unfused(const fk_pipeline* p, const fk_exec_config* c, fk_exec_report* rep) {

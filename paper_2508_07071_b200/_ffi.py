@@ -110,6 +110,8 @@ SIGNATURES = {
     "fk_errc_name": (I32, [I32, C.c_char_p, C.c_size_t]),
     "fk_plane_view": (I32, [C.POINTER(fk_plane), U32, U32, U32, U32, C.POINTER(fk_plane)]),
     "fk_bytes_per_element": (U32, [U32]),
+    "fk_plane_alloc": (I32, [U32, U32, U32, U32, C.POINTER(fk_plane)]),
+    "fk_plane_free": (None, [C.POINTER(fk_plane)]),
     "fk_op_arith": (I32, [U32, U32, P, PP]),
     "fk_op_cast": (I32, [U32, U32, PP]),
     "fk_op_static_loop": (I32, [P, U32, PP]),
@@ -139,6 +141,8 @@ SIGNATURES = {
     "fk_schedule": (I32, [C.POINTER(fk_extent3), C.POINTER(fk_exec_config), C.POINTER(C.c_uint32),
                           C.c_uint64, C.POINTER(C.c_uint64)]),
     "fk_multi_reduce_plane": (I32, [P, C.POINTER(fk_reduce_spec), U32, I32, P, C.POINTER(C.c_uint64)]),
+    "fk_execute_sharded": (I32, [PP, C.POINTER(I32), U32, C.POINTER(fk_exec_config), C.POINTER(fk_exec_report)]),
+    "fk_gather": (I32, [P, I32, C.POINTER(C.c_uint64), PP, C.POINTER(I32), C.POINTER(C.c_uint64), U32, P]),
 }
 
 REDUCE_SUM, REDUCE_MAX, REDUCE_MIN = 0, 1, 2  # fk_reducer (dpp.hpp:32)

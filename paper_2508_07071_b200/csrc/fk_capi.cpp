@@ -1,22 +1,72 @@
 // fk_capi.cpp — the extern "C" boundary (include/fk.h) of libfk_cuda.so.
 // C++ exceptions never cross it: every entry point returns an fk_status and
 // leaves the message / chain position in thread-local storage.
+#include <cuda_runtime.h>
+
 #include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "fk.h"
 #include "fk_core.hpp"
 #include "fk_cuda.h"
 #include "fk_exec.hpp"
 
+// An IOp / pipeline holds the buffers of the fk_plane_alloc planes it
+// references (plane.hpp:97: views and ops share ownership of the buffer).
+using Holds = std::vector<std::shared_ptr<void>>;
 struct fk_iop {
   fk::Op op;
+  Holds hold;
 };
 struct fk_pipeline {
   fk::Pipeline p;
+  Holds hold;
 };
 
 namespace {
+
+// fk_plane_alloc buffers by base address; the registry's reference is the
+// caller's (dropped by fk_plane_free), ops and pipelines add their own.
+struct Buffers {
+  std::mutex mu;
+  std::map<uintptr_t, std::pair<size_t, std::shared_ptr<void>>> by_base;
+};
+Buffers& buffers() {
+  static Buffers* b = new Buffers;  // never destroyed: ops may outlive static teardown
+  return *b;
+}
+std::shared_ptr<void> owner_of(const void* p) {
+  if (!p) return nullptr;
+  Buffers& b = buffers();
+  std::lock_guard<std::mutex> lock(b.mu);
+  if (b.by_base.empty()) return nullptr;
+  const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+  auto it = b.by_base.upper_bound(a);
+  if (it == b.by_base.begin()) return nullptr;
+  --it;
+  return a < it->first + it->second.first ? it->second.second : nullptr;
+}
+void cuda_ok(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();
+  fk::fail(FK_E_CUDA, std::string("CudaError: ") + what + ": " + cudaGetErrorString(e));
+}
+void hold_plane(Holds& h, const fk_plane& pl) {
+  if (auto o = owner_of(pl.data)) h.push_back(std::move(o));
+}
+// every plane an op references (reads, batch reads, writes)
+Holds holds_of(const fk::Op& op) {
+  Holds h;
+  if (fk::is_sample_read(op)) hold_plane(h, op.sample.source);
+  for (const fk::Sample& s : op.planes) hold_plane(h, s.source);
+  for (const fk_plane& d : op.dest) hold_plane(h, d);
+  for (const fk_plane& d : op.wdest) hold_plane(h, d);
+  return h;
+}
 
 thread_local std::string g_err;
 thread_local int32_t g_pos = -1;
@@ -48,7 +98,11 @@ fk_status build(fk_iop** out, Fn&& fn) {
     return FK_E_INVALID_ARGUMENT;
   }
   *out = nullptr;
-  return guard([&] { *out = new fk_iop{fn()}; });
+  return guard([&] {
+    fk::Op op = fn();
+    Holds h = holds_of(op);
+    *out = new fk_iop{std::move(op), std::move(h)};
+  });
 }
 
 const fk::Op& deref(const fk_iop* op, const char* what) {
@@ -86,6 +140,44 @@ fk_status fk_plane_view(const fk_plane* p, uint32_t x0, uint32_t y0, uint32_t w,
     out->width = w;
     out->height = h;
   });
+}
+
+fk_status fk_plane_alloc(uint32_t width, uint32_t height, uint32_t kind, uint32_t row_stride, fk_plane* out) {
+  return guard([&] {  // Plane::alloc, plane.cpp:60-71
+    if (!out) fk::fail(FK_E_INVALID_ARGUMENT, "null output");
+    if (!fk::kind_ok(kind)) fk::fail(FK_E_INVALID_ARGUMENT, "bad kind");
+    const uint32_t rs = row_stride ? row_stride : width;
+    if (width == 0 || height == 0 || rs < width) fk::fail(FK_E_CAPACITY_OVERFLOW, "plane extents must be >= 1");
+    const size_t bytes = size_t(rs) * height * fk::bpe(kind);
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaSuccess) e = cudaMemset(p, 0, bytes);
+    if (e != cudaSuccess) {
+      if (p) cudaFree(p);
+      cudaGetLastError();
+      fk::fail(FK_E_CUDA, std::string("CudaError: plane allocation: ") + cudaGetErrorString(e));
+    }
+    std::shared_ptr<void> buf(p, [](void* q) { cudaFree(q); });
+    {
+      Buffers& b = buffers();
+      std::lock_guard<std::mutex> lock(b.mu);
+      b.by_base[reinterpret_cast<uintptr_t>(p)] = {bytes, std::move(buf)};
+    }
+    *out = fk_plane{p, width, height, rs, kind};
+  });
+}
+void fk_plane_free(fk_plane* pl) {
+  if (!pl || !pl->data) return;
+  std::shared_ptr<void> last;  // released outside the lock
+  {
+    Buffers& b = buffers();
+    std::lock_guard<std::mutex> lock(b.mu);
+    auto it = b.by_base.find(reinterpret_cast<uintptr_t>(pl->data));
+    if (it == b.by_base.end()) return;  // not an fk_plane_alloc base (a view, or already freed)
+    last = std::move(it->second.second);
+    b.by_base.erase(it);
+  }
+  pl->data = nullptr;
 }
 
 fk_status fk_op_arith(uint32_t id, uint32_t kind, const void* value, fk_iop** out) {
@@ -173,7 +265,12 @@ fk_status fk_validate_chain(const fk_iop* const* ops, uint32_t n, fk_pipeline** 
       if (!ops || !ops[i]) fk::fail(FK_E_INVALID_ARGUMENT, "null op", int(i));
       v.push_back(&ops[i]->op);
     }
-    *out = new fk_pipeline{fk::validate_chain(v)};
+    Holds h;
+    for (const fk::Op* o : v) {
+      Holds oh = holds_of(*o);
+      h.insert(h.end(), oh.begin(), oh.end());
+    }
+    *out = new fk_pipeline{fk::validate_chain(v), std::move(h)};
   });
 }
 void fk_pipeline_free(fk_pipeline* p) { delete p; }
@@ -193,6 +290,74 @@ fk_status fk_execute_fused(const fk_pipeline* p, const fk_exec_config* cfg, fk_e
     if (rep) *rep = r;
   });
 }
+fk_status fk_execute_sharded(const fk_pipeline* const* pipelines, const int32_t* devices, uint32_t n,
+                             const fk_exec_config* cfgs, fk_exec_report* reports) {
+  return guard([&] {
+    if (n && (!pipelines || !devices)) fk::fail(FK_E_INVALID_ARGUMENT, "null pipelines / devices");
+    int prev = 0;
+    if (cudaGetDevice(&prev) != cudaSuccess) fk::fail(FK_E_NO_DEVICE, "no CUDA device");
+    struct Restore {
+      int d;
+      ~Restore() { cudaSetDevice(d); }
+    } restore{prev};
+    bool timed = false;
+    for (uint32_t i = 0; i < n; ++i) timed = timed || (cfgs && (cfgs[i].flags & FK_EXEC_TIMED));
+    std::vector<cudaEvent_t> ev(timed ? 2 * n : 0, nullptr);
+    // enqueue every shard before waiting on any (no collective)
+    for (uint32_t i = 0; i < n; ++i) {
+      if (!pipelines[i]) fk::fail(FK_E_INVALID_ARGUMENT, "null pipeline", int(i));
+      cuda_ok(cudaSetDevice(devices[i]), "cudaSetDevice");
+      fk_exec_config c = cfgs ? cfgs[i] : fk_exec_config{0, 8, 8, 0, nullptr};
+      c.flags &= ~FK_EXEC_TIMED;
+      cudaStream_t st = static_cast<cudaStream_t>(c.stream);
+      if (timed) {
+        cuda_ok(cudaEventCreate(&ev[2 * i]), "cudaEventCreate");
+        cuda_ok(cudaEventCreate(&ev[2 * i + 1]), "cudaEventCreate");
+        cuda_ok(cudaEventRecord(ev[2 * i], st), "cudaEventRecord");
+      }
+      const fk_exec_report r = fk::execute_fused(pipelines[i]->p, &c);
+      if (timed) cuda_ok(cudaEventRecord(ev[2 * i + 1], st), "cudaEventRecord");
+      if (reports) reports[i] = r;
+    }
+    for (uint32_t i = 0; timed && i < n; ++i) {
+      cuda_ok(cudaSetDevice(devices[i]), "cudaSetDevice");
+      cuda_ok(cudaEventSynchronize(ev[2 * i + 1]), "cudaEventSynchronize");
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[2 * i], ev[2 * i + 1]);
+      if (reports) reports[i].device_ms = ms;
+      cudaEventDestroy(ev[2 * i]);
+      cudaEventDestroy(ev[2 * i + 1]);
+    }
+  });
+}
+
+fk_status fk_gather(void* dst, int32_t dst_device, const uint64_t* dst_offsets, const void* const* srcs,
+                    const int32_t* src_devices, const uint64_t* bytes, uint32_t n, void* stream) {
+  return guard([&] {
+    if (n && (!dst || !dst_offsets || !srcs || !src_devices || !bytes)) fk::fail(FK_E_INVALID_ARGUMENT, "null argument");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    for (uint32_t i = 0; i < n; ++i) {
+      if (src_devices[i] != dst_device) {  // peer access over NVLink when the pair supports it
+        int can = 0;
+        cudaDeviceCanAccessPeer(&can, dst_device, src_devices[i]);
+        if (can) {
+          int prev = 0;
+          cudaGetDevice(&prev);
+          cudaSetDevice(dst_device);
+          const cudaError_t e = cudaDeviceEnablePeerAccess(src_devices[i], 0);
+          if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            cuda_ok(e, "cudaDeviceEnablePeerAccess");
+          cudaGetLastError();
+          cudaSetDevice(prev);
+        }
+      }
+      cuda_ok(cudaMemcpyPeerAsync(static_cast<uint8_t*>(dst) + dst_offsets[i], dst_device, srcs[i],
+                                         src_devices[i], bytes[i], st),
+                     "cudaMemcpyPeerAsync");
+    }
+  });
+}
+
 fk_status fk_execute_unfused(const fk_pipeline* p, const fk_exec_config* cfg, fk_exec_report* rep) {
   return guard([&] {
     if (!p) fk::fail(FK_E_INVALID_ARGUMENT, "null pipeline");

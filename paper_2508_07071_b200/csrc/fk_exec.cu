@@ -307,7 +307,8 @@ WalkRow walk_row(uint32_t y, uint32_t rect_h, uint32_t out_h) {
   WalkRow r{};
   const bool same = iy0 == iy1;
   r.r1 = iy1 | (same ? kWalkSame : 0u) | ((same || (ny * 128) % den == 0) ? kWalkExactRow : 0u);
-  r.fy = same ? 0.0f : float(double(ny) / double(den));
+  r.fy = same ? 1.0f : float(double(ny) / double(den));  // clamped: both taps are row r1 (fk_walk: Ha + (Hb - Ha) 1 = Hb)
+  r.fy_ = r.fy;
   return r;
 }
 
@@ -422,7 +423,7 @@ void build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
     if (r == row_at.end()) {
       r = row_at.emplace(s.rect_h, uint32_t(rows.size())).first;
       for (uint32_t y = 0; y < H; ++y) rows.push_back(walk_row(y, s.rect_h, H));
-      rows.push_back(WalkRow{kWalkRowMask, 0.0f});  // sentinel: the walk reads one row ahead
+      rows.push_back(WalkRow{kWalkRowMask, 0, 0.0f, 0.0f});  // sentinel: the walk reads one row ahead
     }
     auto c = col_at.find(s.rect_w);
     if (c == col_at.end()) {
@@ -493,7 +494,6 @@ void build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   // of 2, 4 or 8 bytes (the smallest whose 256-element box holds a staged row)
   // over [0, ceil(3 (x0 + rect_w) / elem)): the last element of a row may
   // extend past the crop, so that byte range must be readable in its last row
-  row_bytes = (row_bytes + 31) & ~31u;  // 4-row boxes stay 128-byte aligned in shared memory
   const uint32_t elem = row_bytes <= 512 ? 2 : row_bytes <= 1024 ? 4 : 8;
   if (!ok || units.empty() || row_bytes > 256 * elem) return;
   if (walk_smem_bytes(row_bytes, band_rows) > 200 * 1024) return;

@@ -54,15 +54,47 @@ namespace {
 
 constexpr float kRound = 12582912.0f;        // 1.5 * 2^23: x + kRound rounds x to an integer (ties to even)
 
+__host__ __device__ constexpr bool div2(uint32_t sig, int k) { return (sig >> (kWalkDiv2 + k)) & 1u; }
+
 // The chain's constants for input lane m, op k, as pairs: c, and for a division
 // either (r_hi, r_lo) [two-op form] or (RN(1/c), -c) [three-op form].
+#ifndef FK_WALK_PEEL
+#define FK_WALK_PEEL 1
+#endif
+#ifndef FK_WALK_KREG
+#define FK_WALK_KREG 0  // 1: chain constants held in registers (measured slower: 1.46 vs 1.39 ms on C5)
+#endif
+#if FK_WALK_KREG
+template <uint32_t SIG>
+struct KInl {  // the chain's constants held in registers (only those the chain uses)
+  uint64_t cc[4][3], hh[4][3], ll[4][3];
+  uint64_t z;  // runtime -0 pair (fk_pack2.cuh)
+  __device__ __forceinline__ KInl(const WalkPlan& P, uint64_t negz) : z(negz) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int m = 0; m < 3; ++m) {
+        const bool div = k < sig_n(SIG) && sig_fn(SIG, k) == AF_DIV;
+        cc[k][m] = k < sig_n(SIG) && !(div && (div2(SIG, k) || sig_fast(SIG, k))) ? p2::of(P.kc[k][m]) : 0;
+        hh[k][m] = div ? p2::of(P.kh[k][m]) : 0;
+        ll[k][m] = div ? p2::of(P.kl[k][m]) : 0;
+      }
+  }
+  __device__ __forceinline__ uint64_t c(int k, int m) const { return cc[k][m]; }
+  __device__ __forceinline__ uint64_t h(int k, int m) const { return hh[k][m]; }
+  __device__ __forceinline__ uint64_t l(int k, int m) const { return ll[k][m]; }
+};
+#else
+template <uint32_t SIG>
 struct KInl {
   const WalkPlan& P;
   uint64_t z;  // runtime -0 pair (fk_pack2.cuh)
+  __device__ __forceinline__ KInl(const WalkPlan& Pp, uint64_t negz) : P(Pp), z(negz) {}
   __device__ __forceinline__ uint64_t c(int k, int m) const { return p2::of(P.kc[k][m]); }
   __device__ __forceinline__ uint64_t h(int k, int m) const { return p2::of(P.kh[k][m]); }
   __device__ __forceinline__ uint64_t l(int k, int m) const { return p2::of(P.kl[k][m]); }
 };
+#endif
 template <uint32_t SIG>
 struct KReg {
   uint64_t cc[4][3], hh[4][3], ll[4][3];
@@ -87,7 +119,6 @@ struct KReg {
   __device__ __forceinline__ uint64_t l(int k, int m) const { return ll[k][m]; }
 };
 
-__host__ __device__ constexpr bool div2(uint32_t sig, int k) { return (sig >> (kWalkDiv2 + k)) & 1u; }
 
 // The registered chain on a column pair: the reference's arith ops
 // (ops.cpp:88-159), same IEEE ops in the same order; divisions in a
@@ -194,14 +225,33 @@ __device__ __forceinline__ void tma_rows(uint32_t dst, uint64_t map, uint32_t x,
           "r"(dst), "l"(map), "r"(x), "r"(y), "r"(mbar)
       : "memory");
 }
+// One elected lane: expect `tx` bytes on mbar, copy half 0's box to dst and, if
+// off1 != 0, half 1's box to dst + off1 (all operands warp-uniform).
+__device__ __forceinline__ void tma_group(uint32_t dst, uint64_t m0, uint32_t x0, uint64_t m1, uint32_t x1, uint32_t y,
+                                          uint32_t mbar, uint32_t tx, uint32_t off1) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "elect.sync _|p, 0xffffffff;\n\t"
+      "setp.ne.and.u32 q, %8, 0, p;\n\t"
+      "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%6], %7;\n\t"
+      "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %5}], [%6];\n\t"
+      "@q cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%9], [%3, {%4, %5}], [%6];\n\t"
+      "}" ::"r"(dst),
+      "l"(m0), "r"(x0), "l"(m1), "r"(x1), "r"(y), "r"(mbar), "r"(tx), "r"(off1), "r"(dst + off1)
+      : "memory");
+}
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
 }
-__device__ __forceinline__ WalkRow ld_row(const WalkRow* p) {
-  const uint2 v = __ldg(reinterpret_cast<const uint2*>(p));
-  return WalkRow{v.x, __uint_as_float(v.y)};
+struct RowReg {  // a WalkRow in registers, fy as a packed pair
+  uint32_t r1;
+  uint64_t fy2;
+};
+__device__ __forceinline__ RowReg ld_row(const WalkRow* p) {
+  const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+  return RowReg{v.x, (uint64_t(v.w) << 32) | v.z};
 }
 // base + a * b in one IMAD.WIDE (the compiler would share a * b across the three planes)
 __device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t base) {
@@ -240,7 +290,8 @@ struct StageArgs {
   uint32_t two;         // half 1 present
   uint32_t pad;
 };
-__host__ __device__ constexpr uint32_t walk_ring_bytes(uint32_t rb) { return kWalkSlots * 2 * kWalkGroup * rb; }
+__host__ __device__ constexpr uint32_t walk_half_bytes(uint32_t rb) { return (kWalkGroup * rb + 127) / 128 * 128; }
+__host__ __device__ constexpr uint32_t walk_ring_bytes(uint32_t rb) { return kWalkSlots * 2 * walk_half_bytes(rb); }
 __host__ __device__ constexpr uint32_t walk_warp_bytes(uint32_t rb, uint32_t max_rows) {
   return (walk_ring_bytes(rb) + 8 * kWalkSlots + uint32_t(sizeof(StageArgs)) + 4 * max_rows + 16 + 127) / 128 * 128;
 }
@@ -253,7 +304,7 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   const uint32_t u = blockIdx.x * kWalkWarps + wi;
   if (u >= P.n_units) return;  // the whole warp: no CTA-wide synchronisation follows
   const WalkUnit U = P.units[u];
-  const uint32_t RB = P.row_bytes, HB = kWalkGroup * RB, GB = 2 * HB;
+  const uint32_t RB = P.row_bytes, HB = walk_half_bytes(RB), GB = 2 * HB;
   unsigned char* wbase = smem + wi * walk_warp_bytes(RB, P.max_rows);
   const uint32_t ring = uint32_t(__cvta_generic_to_shared(wbase));
   const uint32_t bar = ring + kWalkSlots * GB;
@@ -289,10 +340,10 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
 #pragma unroll
   for (int m = 0; m < 3; ++m) dst[m] = A.dst[m] + 4ull * x;
   const uint32_t dpitch = A.dpitch;
-  using KS = typename std::conditional<PERZ, KReg<SIG>, KInl>::type;
+  using KS = typename std::conditional<PERZ, KReg<SIG>, KInl<SIG>>::type;
   const KS ks = [&]() {
     if constexpr (PERZ) return KReg<SIG>(P.kz + 12ull * A.kz, P.negz);
-    else return KInl{P, P.negz};
+    else return KInl<SIG>(P, P.negz);
   }();
 
   // lane 0 stages group g (source rows r_first + 4 g ...) into ring slot g % 2,
@@ -308,31 +359,40 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
     t.two = U.n[1] != 0;
     *sa = t;
   }
+  // Called by the whole (converged) warp: the arguments are made warp-uniform
+  // with shuffles, so one elected lane issues the copies straight from uniform
+  // registers (no per-lane issue loop).
   auto stage = [&](uint32_t g) {
     const StageArgs t = *sa;
-    const uint32_t slot = g % kWalkSlots, r = r_first + g * kWalkGroup;
-    mbar_expect_tx(bar + 8 * slot, t.two ? GB : HB);
-    tma_rows(ring + slot * GB, t.map0, t.bx0, r, bar + 8 * slot);
-    if (t.two) tma_rows(ring + slot * GB + HB, t.map1, t.bx1, r, bar + 8 * slot);
+    const uint64_t m0 = __shfl_sync(0xffffffffu, t.map0, 0), m1 = __shfl_sync(0xffffffffu, t.map1, 0);
+    const uint32_t bx0 = __shfl_sync(0xffffffffu, t.bx0, 0), bx1 = __shfl_sync(0xffffffffu, t.bx1, 0);
+    const uint32_t two = __shfl_sync(0xffffffffu, t.two, 0);
+    const uint32_t slot = g % kWalkSlots;
+    const uint32_t r = __shfl_sync(0xffffffffu, r_first, 0) + g * kWalkGroup;
+    const uint32_t mb = __shfl_sync(0xffffffffu, bar, 0) + 8 * slot;
+    const uint32_t dst = __shfl_sync(0xffffffffu, ring, 0) + slot * GB;
+    const uint32_t box = kWalkGroup * RB;  // bytes one box delivers (zero-filled outside the crop)
+    tma_group(dst, m0, bx0, m1, bx1, r, mb, two ? 2 * box : box, two ? HB : 0u);
   };
   if (lane == 0) {
 #pragma unroll
     for (uint32_t i = 0; i < kWalkSlots; ++i) mbar_init(bar + 8 * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (uint32_t g = 0; g < kWalkSlots && g < ngroups; ++g) stage(g);
   }
   __syncwarp();
+  for (uint32_t g = 0; g < kWalkSlots && g < ngroups; ++g) stage(g);
   const uint32_t y_hi = U.y_hi, y_lo = U.y_lo;
   uint32_t y = y_lo;
   const WalkRow* rp = P.rows + U.rowtab + y;  // row table, walked with y
-  WalkRow R = ld_row(rp);
+  RowReg R = ld_row(rp);
   for (uint32_t i = lane; i < y_hi - y_lo; i += 32) fixm[i] = 0;
-  bool any_fix = false;  // warp-uniform
+  __syncwarp();
 
-  // finish output row y from the H rows of its two source rows
-  auto finish = [&](const float (&Ha)[2][3], const float (&Hb)[2][3]) {
-    const uint64_t fy2 = p2::pack(R.fy, R.fy);
-    const bool exact_row = R.r1 & kWalkExactRow;
+  // finish output row y from the H rows of its two source rows (a clamped row
+  // has fy = 1: Ha + (Hb - Ha) * 1 == Hb exactly)
+  auto finish = [&](const float (&Ha)[2][3], const float (&Hb)[2][3], const RowReg& Rw) {
+    const uint64_t fy2 = Rw.fy2;
+    const bool exact_row = Rw.r1 & kWalkExactRow;
     const float t0 = exact_row ? tc[0] : kWalkThr, t1 = exact_row ? tc[1] : kWalkThr;
     bool flag = false;
 #pragma unroll
@@ -346,31 +406,34 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
       const uint64_t o = chain2<SIG>(k, ks, m);
       if (active) st_cs2(mad_wide(y, dpitch, dst[m]), o);
     }
-    const uint32_t bal = __ballot_sync(0xffffffffu, flag && active);
-    if (bal) {  // rare: note the row's flagged lanes
-      if (lane == 0) fixm[y - y_lo] = bal;
-      any_fix = true;
-    }
+    if (flag && active) atomicOr(fixm + (y - y_lo), 1u << lane);  // rare: fixed after the walk
   };
 
   float HA[2][3], HB2[2][3];
   // visit k (row staged at `row`): H into Hn, then every output row it completes
   auto visit = [&](uint32_t k, uint32_t row, float (&Hn)[2][3], float (&Hp)[2][3]) {
     h_row(row, w, sh, wts, Hn);
+#if !FK_WALK_PEEL
     if (k == 0) {
 #pragma unroll
       for (int i = 0; i < 2; ++i)
 #pragma unroll
         for (int m = 0; m < 3; ++m) Hp[i][m] = Hn[i][m];
     }
+#endif
     const uint32_t r = r_first + k;
     while (y < y_hi && (R.r1 & kWalkRowMask) == r) {
-      if (R.r1 & kWalkSame) finish(Hn, Hn);
-      else finish(Hp, Hn);
+      const RowReg Rc = R;
+      R = ld_row(++rp);  // the next row's entry, in flight during the finish (sentinel past out_h)
+      finish(Hp, Hn, Rc);
       ++y;
-      R = ld_row(++rp);  // the table has a sentinel row past out_h
     }
   };
+  // visit 0's "previous" row is row 0 itself (only a clamped row completes there)
+#if FK_WALK_PEEL
+  mbar_wait(bar, 0);
+  h_row(ring, w, sh, wts, HB2);
+#endif
   for (uint32_t g = 0; g < ngroups; ++g) {
     const uint32_t slot = g % kWalkSlots;
     mbar_wait(bar + 8 * slot, (g / kWalkSlots) & 1u);
@@ -379,18 +442,18 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
       const uint32_t k = g * kWalkGroup + q, row = ring + slot * GB + q * RB;
       if (k >= nvis) break;
       visit(k, row, HA, HB2);
-      if (k + 1 < nvis) visit(k + 1, row + RB, HB2, HA);
-      if (k + 2 < nvis) visit(k + 2, row + 2 * RB, HA, HB2);
-      if (k + 3 < nvis) visit(k + 3, row + 3 * RB, HB2, HA);
+      if (k + 1 < nvis && q + 1 < kWalkGroup) visit(k + 1, row + RB, HB2, HA);
+      if (k + 2 < nvis && q + 2 < kWalkGroup) visit(k + 2, row + 2 * RB, HA, HB2);
+      if (k + 3 < nvis && q + 3 < kWalkGroup) visit(k + 3, row + 3 * RB, HB2, HA);
     }
     __syncwarp();  // every lane is done with the slot
-    if (lane == 0 && g + kWalkSlots < ngroups) stage(g + kWalkSlots);
+    if (g + kWalkSlots < ngroups) stage(g + kWalkSlots);
   }
   // values near a rounding boundary (rare), recomputed in the reference's
   // arithmetic: the flagged (row, lane) pairs are dealt to the warp's lanes,
   // 32 at a time, so the double-precision path runs with full warps
-  if (any_fix) {
-    __syncwarp();  // the fast values and the masks are stored
+  __syncwarp();  // the fast values and the masks are stored
+  {
     uint32_t pend = 0, my_row = 0, my_owner = 0;
     for (uint32_t i0 = 0; i0 < y_hi - y_lo; i0 += 32) {
       const uint32_t mi = i0 + lane < y_hi - y_lo ? fixm[i0 + lane] : 0u;

@@ -15,10 +15,16 @@
 namespace fk {
 
 constexpr uint32_t kWalkWarps = 4;               // warps per CTA (independent: no CTA barrier)
-constexpr uint32_t kWalkGroup = 8;               // source rows per TMA box (one copy per 8 visits)
+#ifndef FK_WALK_GROUP
+#define FK_WALK_GROUP 6  // 6 vs 8: 1.346 vs 1.366 ms on C5 (smaller ring)
+#endif
+constexpr uint32_t kWalkGroup = FK_WALK_GROUP;   // source rows per TMA box (one copy per group of visits; even)
 constexpr uint32_t kWalkSlots = 2;               // box slots per half in the ring (8-16 rows staged ahead)
 constexpr uint32_t kWalkHalfLanes = 16;          // lanes per half-warp strip (2 output columns per lane)
-constexpr uint32_t kWalkMaxRows = 256;           // output rows per unit (bounds the fix list)
+#ifndef FK_WALK_MAXROWS
+#define FK_WALK_MAXROWS 112  // 112-row bands: twice the units of whole-plane walks, a shorter tail
+#endif
+constexpr uint32_t kWalkMaxRows = FK_WALK_MAXROWS;  // output rows per unit (bounds the fix masks)
 constexpr uint32_t kWalkBias = 0x4B000000u;      // bit pattern of 2^23: H values are biased floats
 constexpr float kWalkThr = 0.5f - 1.0f / 8192.0f;  // exact-result filter: 0.5 - E, E = 2^-13
 
@@ -41,11 +47,13 @@ struct WalkCol {
 };
 // One output row y of a (rect_h, out_h) table: the row completes when the walk
 // has visited source row r1 (relative to y0, clamped); r0 = r1 - 1, or r0 = r1
-// at a clamped edge (then fy = 0). Each table ends with a sentinel row (r1 =
+// at a clamped edge (then fy = 1: the lerp of the rows r1 - 1 and r1 with
+// weight 1 is row r1 exactly). Each table ends with a sentinel row (r1 =
 // kWalkRowMask, never visited) so the walk may read one row past out_h.
 struct WalkRow {
   uint32_t r1;    // r1 | same << 31 (r0 == r1) | exact << 30 (fy = j / 2^m, m <= 7, or same)
-  float fy;       // RN(ny / den) (0 when clamped)
+  uint32_t pad;
+  float fy, fy_;  // RN(ny / den) (1 when clamped), twice: the FFMA2 operand pair
 };
 constexpr uint32_t kWalkSame = 0x80000000u;
 constexpr uint32_t kWalkExactRow = 0x40000000u;

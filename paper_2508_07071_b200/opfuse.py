@@ -145,6 +145,56 @@ class Plane:
                 f"on {self.storage.device})")
 
 
+class RawPlane:
+    """A bare fk_plane view (no Python-side owner)."""
+
+    def __init__(self, raw: "_ffi.fk_plane"):
+        self._raw = raw
+        self.width, self.height, self.row_stride, self.kind = raw.width, raw.height, raw.row_stride, raw.kind
+
+    def c(self) -> "_ffi.fk_plane":
+        return self._raw
+
+
+class SharedPlane:
+    """A plane from fk_plane_alloc (Plane::alloc, plane.cpp:60-71): the buffer is
+    shared with every IOp / pipeline built from it or a view of it, like the
+    reference's shared_ptr<TensorBuffer> (plane.hpp:97); free() (or garbage
+    collection) only drops this handle's reference."""
+
+    def __init__(self, lib: "Library", raw: "_ffi.fk_plane"):
+        self._lib, self._raw = lib, raw
+        self.width, self.height, self.row_stride, self.kind = raw.width, raw.height, raw.row_stride, raw.kind
+
+    @property
+    def bpe(self) -> int:
+        return BYTES_PER_ELEMENT[self.kind]
+
+    @property
+    def data_ptr(self) -> int:
+        return int(self._raw.data or 0)
+
+    def c(self) -> "_ffi.fk_plane":
+        return _ffi.fk_plane(self._raw.data, self.width, self.height, self.row_stride, self.kind)
+
+    def view(self, x0: int, y0: int, width: int, height: int) -> "RawPlane":
+        """fk_plane_view: a zero-copy sub-view (it does not keep the buffer alive by
+        itself; IOps built from it do)."""
+        out = _ffi.fk_plane()
+        self._lib._check(self._lib._c.fk_plane_view(C.byref(self._raw), x0, y0, width, height, C.byref(out)))
+        return RawPlane(out)
+
+    def free(self):
+        if self._raw.data:
+            self._lib._c.fk_plane_free(C.byref(self._raw))
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 def kind_of_array(arr: np.ndarray) -> int:
     packed = arr.ndim == 3
     if packed and arr.shape[2] != 3:
@@ -298,6 +348,12 @@ class Library:
         rs = width if row_stride is None else row_stride
         return Plane(self._storage(rs * height * BYTES_PER_ELEMENT[kind]), 0, width, height, rs, kind)
 
+    def plane_alloc_shared(self, width: int, height: int, kind: int, row_stride: int = 0) -> SharedPlane:
+        """fk_plane_alloc: a library-owned plane whose buffer IOps keep alive (plane.hpp:97)."""
+        out = _ffi.fk_plane()
+        self._check(self._c.fk_plane_alloc(width, height, kind, row_stride, C.byref(out)))
+        return SharedPlane(self, out)
+
     def plane_from_numpy(self, arr: np.ndarray, kind: int | None = None, row_stride: int | None = None) -> Plane:
         import torch
         arr = np.ascontiguousarray(arr)
@@ -400,6 +456,28 @@ class Library:
 
     def execute_unfused(self, pipeline, cfg: ExecConfig | None = None) -> ExecReport:
         return self._exec(self._c.fk_execute_unfused, pipeline, cfg)
+
+    def execute_sharded(self, pipelines, devices, cfgs=None):
+        """fk_execute_sharded: pipelines[i] (a batch shard) on devices[i], all enqueued
+        before any wait; returns one ExecReport per shard."""
+        n = len(pipelines)
+        arr = (C.c_void_p * max(n, 1))(*(p._ptr.value for p in pipelines))
+        devs = (C.c_int32 * max(n, 1))(*devices)
+        cs = None
+        if cfgs is not None:
+            cs = (_ffi.fk_exec_config * max(n, 1))(*(c.c() for c in cfgs))
+        reps = (_ffi.fk_exec_report * max(n, 1))()
+        self._check(self._c.fk_execute_sharded(arr, devs, n, cs, reps))
+        return [ExecReport.from_c(reps[i]) for i in range(n)]
+
+    def gather(self, dst_ptr: int, dst_device: int, parts, stream: int | None = None):
+        """fk_gather: parts = [(dst_offset, src_ptr, src_device, nbytes), ...] peer copies."""
+        n = len(parts)
+        offs = (C.c_uint64 * max(n, 1))(*(p[0] for p in parts))
+        srcs = (C.c_void_p * max(n, 1))(*(p[1] for p in parts))
+        devs = (C.c_int32 * max(n, 1))(*(p[2] for p in parts))
+        nb = (C.c_uint64 * max(n, 1))(*(p[3] for p in parts))
+        self._check(self._c.fk_gather(dst_ptr, dst_device, offs, srcs, devs, nb, n, stream))
 
     def last_kernel(self) -> str:
         """Kernel family of this thread's last execute / reduce (CUDA backend only)."""

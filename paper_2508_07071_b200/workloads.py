@@ -147,6 +147,26 @@ def c2(lib: Library, seed: int = 42) -> Workload:
                     {"crops": 50, "out": "64x128", "chain": "crop->resize->SwapRB->f32->sub->div->split"})
 
 
+def c4_reference_planes(lib: Library, n: int, seed: int = 42, n_frames: int = 16) -> list:
+    """C4's crops as n single-plane pipelines, each with its own normalize
+    constants: the reference cannot express per-plane constants in one batch,
+    so its C4 is one pipeline per crop (the bench.cpp:199-202 pattern). Same
+    frames, rects and constants as crops_224(..., per_crop_norm=True)."""
+    rng = np.random.default_rng(seed)
+    frames = [lib.plane_from_numpy(rng.integers(0, 256, (1080, 1920, 3), dtype=np.uint8))
+              for _ in range(n_frames)]
+    rects = crop_rects(n, np.random.default_rng(7), 112, 448)
+    jr = np.random.default_rng(11)
+    means = [tuple(float(np.float32(m + jr.normal(0, 2.0))) for m in MEAN) for _ in range(n)]
+    stds = [tuple(float(np.float32(s + jr.normal(0, 1.0))) for s in STD) for _ in range(n)]
+    out = []
+    for z in range(n):
+        p, o = crops_pipeline(lib, frames, [rects[z]], lambda _z, z=z: z % n_frames, 224, 224, swap_rb=False,
+                              means=means[z], stds=stds[z])
+        out.append((p, o))
+    return out, frames
+
+
 def crops_224(lib: Library, n: int, per_crop_norm: bool, seed: int = 42, n_frames: int = 16,
               name: str = "C5", first: int = 0) -> Workload:
     """C4/C5: crops of 16 frames (crop z from frame z % 16), w,h in [112, 448] -> 224x224."""

@@ -88,3 +88,40 @@ def test_two_rank_gloo_sharding_matches_unsharded_run():
         p.join(timeout=60)
         assert p.exitcode == 0
     assert same and planes == n and max_ok and points == n * 24 * 16
+
+
+def test_execute_sharded_cpu_backends(oracle, reference):
+    """fk_execute_sharded on the CPU backends runs the shards one after another:
+    the shard outputs concatenate to the unsharded output."""
+    import torch
+    from paper_2508_07071_b200 import workloads as wl
+    for lib in (oracle,):
+        n, shards = 10, 3
+        whole = wl.crops_224(lib, n, per_crop_norm=False)
+        lib.execute_fused(whole.pipeline)
+        parts = [wl.crops_224(lib, hi - lo, per_crop_norm=False, first=lo)
+                 for lo, hi in (shard_range(n, r, shards) for r in range(shards))]
+        reps = lib.execute_sharded([p.pipeline for p in parts], [0] * shards)
+        assert len(reps) == shards
+        assert torch.equal(torch.cat([p.outputs[0] for p in parts]), whole.outputs[0])
+        dst = torch.empty_like(whole.outputs[0])
+        off, plan = 0, []
+        for p in parts:
+            plan.append((off, p.outputs[0].data_ptr(), 0, p.outputs[0].numel()))
+            off += p.outputs[0].numel()
+        lib.gather(dst.data_ptr(), 0, plan)
+        assert torch.equal(dst, whole.outputs[0])
+
+
+def test_plane_alloc_cpu_backends(oracle, reference):
+    from paper_2508_07071_b200._ffi import F32X3
+    from paper_2508_07071_b200.opfuse import OpfuseError
+    for lib in (oracle, reference):
+        p = lib.plane_alloc_shared(5, 3, F32X3)
+        assert p.data_ptr != 0 and p.row_stride == 5
+        v = p.view(1, 1, 2, 2)
+        assert v.width == 2 and v.c().data == p.data_ptr + (5 + 1) * 12
+        p.free()
+        assert p.data_ptr == 0
+        with pytest.raises(OpfuseError):
+            lib.plane_alloc_shared(0, 3, F32X3)
