@@ -21,6 +21,7 @@
 
 #include "fk_core.hpp"
 #include "fk_pack2.cuh"
+#include "fk_stream.hpp"
 #include "fk_walk.hpp"
 #include "fk_reduce.hpp"
 #include "fk_exec.hpp"
@@ -204,6 +205,16 @@ struct DeviceProgram {
   bool walk_perz = false;        // per-plane chain constants (BatchArith or per-plane lane swaps)
   uint32_t walk_sig = 0;
   WalkPlan walk{};               // units, tables, inline constants (reads set at launch)
+  // roofline-grade unfused comparator (fk_stream.cu): pass 0 = fk_walk over the
+  // first op into a planar intermediate, or a stream pass; then one stream pass
+  // per op and the write pass (src / dst pointers set per execute)
+  bool unf_fast = false;
+  bool unf_walk = false;
+  WalkPlan unf_walk_plan{};
+  uint32_t unf_walk_sig = 0;
+  bool unf_walk_perz = false;
+  std::vector<StreamPass> unf_pass;  // [0, n]: pass i (pass 0 unused when unf_walk), n = the write pass
+  std::vector<uint64_t> unf_bytes;   // intermediate bytes after pass i
 
   ~DeviceProgram() {
     for (void* p : {static_cast<void*>(d_table), static_cast<void*>(d_reads), static_cast<void*>(d_writes),
@@ -379,13 +390,13 @@ bool recip2_div_exact(const std::vector<DOp>& arith, size_t k, const std::map<ui
 // of the output size) of a u8x3 frame with 16-byte aligned rows, an AFFINE
 // chain, a split write of three f32 planes sharing one 8-byte multiple pitch,
 // an even output width.
-void build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& arith, uint32_t sig,
-                const std::vector<DWrite>& writes) {
+bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& arith, uint32_t sig,
+                const std::vector<DWrite>& writes, WalkPlan& P, uint32_t& wsig_out, bool& perz_out) {
   const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
   const uint32_t wid = p.write.id == FK_OP_BATCH_WRITE ? p.write.w_inner : p.write.id;
   if (!dp.affine_ok || dp.resample_lanes != 3 || wid != FK_OP_SPLIT_WRITE || B == 0 || W % 2 || W == 0 || H == 0 ||
       W > 65534 || H > 65535 || lane_kind(uint32_t(p.write.in_kind)) != FK_F32)
-    return;
+    return false;
   bool ok = true;
   for (const DSample& s : dp.reads) {
     // a crop without resize (rect == out, resizing() false) is the bilinear walk with fx = fy = 0
@@ -396,7 +407,7 @@ void build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   for (const DWrite& w : writes)
     ok = ok && (w.flags & WF_ACTIVE) && w.pitch[0] == w.pitch[1] && w.pitch[0] == w.pitch[2] &&
          (w.pitch[0] & 7) == 0 && w.pitch[0] < (1ull << 32) && ((w.dst[0] | w.dst[1] | w.dst[2]) & 7) == 0;
-  if (!ok) return;
+  if (!ok) return false;
   // chain: the AFFINE signature with the verified division forms
   uint32_t fn[4] = {0, 0, 0, 0}, fast = 0, two = 0;
   for (size_t k = 0; k < arith.size(); ++k) {
@@ -408,7 +419,7 @@ void build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   uint32_t wsig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast) | (two << kWalkDiv2);
   if (!walk_registered(wsig)) wsig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], fast);
   if (!walk_registered(wsig)) wsig = sig_make(int(arith.size()), fn[0], fn[1], fn[2], fn[3], 0);
-  if (!walk_registered(wsig)) return;
+  if (!walk_registered(wsig)) return false;
 
   // tables: one per distinct crop height / width (the out extents are uniform)
   std::vector<WalkRow> rows;
@@ -495,8 +506,8 @@ void build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   // over [0, ceil(3 (x0 + rect_w) / elem)): the last element of a row may
   // extend past the crop, so that byte range must be readable in its last row
   const uint32_t elem = row_bytes <= 512 ? 2 : row_bytes <= 1024 ? 4 : 8;
-  if (!ok || units.empty() || row_bytes > 256 * elem) return;
-  if (walk_smem_bytes(row_bytes, band_rows) > 200 * 1024) return;
+  if (!ok || units.empty() || row_bytes > 256 * elem) return false;
+  if (walk_smem_bytes(row_bytes, band_rows) > 200 * 1024) return false;
   std::vector<CUtensorMap> maps(B);
   for (uint32_t z = 0; z < B && ok; ++z) {
     const DSample& s = dp.reads[z];
@@ -507,7 +518,7 @@ void build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   }
   for (WalkUnit& u : units)
     for (int h = 0; h < 2; ++h) u.bx[h] = uint16_t(u.bx[h] * 2 / elem);  // bx was in 2-byte elements
-  if (!ok) return;
+  if (!ok) return false;
   // units of one source frame back to back (the frame stays L2-resident while
   // its crops run), longest first within a frame (walk cost ~ visits + rows)
   std::stable_sort(units.begin(), units.end(), [&](const WalkUnit& a, const WalkUnit& b) {
@@ -531,7 +542,6 @@ void build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
     h = 1.0f / c;
     l = (two >> k) & 1u ? float(1.0 / double(c) - double(h)) : -c;
   };
-  WalkPlan& P = dp.walk;
   P = WalkPlan{};
   if (perz) {
     std::vector<float4> kz(size_t(B) * 12, make_float4(0, 0, 0, 0));
@@ -568,9 +578,101 @@ void build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   P.elem = elem;
   P.negz = kNegZero2;
   P.max_rows = band_rows;
-  dp.walk_ok = true;
-  dp.walk_perz = perz;
-  dp.walk_sig = wsig;
+  wsig_out = wsig;
+  perz_out = perz;
+  return true;
+}
+
+// The fast unfused comparator's passes (execute_unfused, executor.cpp:134-217),
+// when every pass is streamable: f32 / f32x3 arithmetic, a final Cast f32 ->
+// u8 on one lane, a split / per-thread write of the last intermediate; pass 0
+// through fk_walk (crop batches) or a stream over contiguous f32 sources.
+void build_unfused(DeviceProgram& dp, const Pipeline& p, const std::vector<DWrite>& writes) {
+  const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
+  const size_t n = p.compute.size();
+  const uint64_t pts = uint64_t(W) * H;
+  if (n == 0 || W % 4 || pts % 4 || pts * B * 3 / 4 >= (uint64_t(1) << 32) || dp.reads.empty()) return;
+  const DOp* ops = dp.table.data() + dp.n_fused;  // the 1:1 program
+  auto plane_div = [&](uint32_t nl) { return make_fastdiv(uint32_t(pts / 4)); };
+  std::vector<StreamPass> passes(n + 1);
+  std::vector<uint64_t> bytes(n);
+  uint32_t kind = uint32_t(p.read.out_kind);
+  for (size_t i = 0; i < n; ++i) {
+    const DOp& d = ops[i];
+    const uint32_t out = uint32_t(p.compute[i].out_kind);
+    StreamPass& S = passes[i];
+    S = StreamPass{};
+    S.nl = uint32_t(lanes_of(kind));
+    S.chunks = pts * B * S.nl / 4;
+    S.plane_chunks = plane_div(S.nl);
+    S.negz = kNegZero2;
+    S.repeat = 1;
+    if (d.cls == OC_ARITH && lane_kind(kind) == FK_F32 && out == kind) {
+      S.op = SP_ARITH;
+      S.fn = d.fn;
+      S.repeat = d.repeat;
+      for (int l = 0; l < 3; ++l) S.c[l] = f32_bits(d.c[d.nl == 3 ? l : 0]);
+      S.per_z = reinterpret_cast<const uint64_t*>(d.per_z);
+      S.per_z_n = d.per_z_n;
+    } else if (d.cls == OC_NOP && lane_kind(kind) == FK_F32 && out == kind) {
+      S.op = SP_ARITH;  // an identity cast: a copy pass
+      S.fn = AF_ADD;
+      S.repeat = 0;
+    } else if (d.cls == OC_CAST && kind == FK_F32 && out == FK_U8) {
+      S.op = SP_TO_U8;
+    } else {
+      return;
+    }
+    bytes[i] = pts * B * bpe(out);
+    kind = out;
+  }
+  // the write pass: the last intermediate through the write op
+  const uint32_t wid = p.write.id == FK_OP_BATCH_WRITE ? p.write.w_inner : p.write.id;
+  StreamPass& F = passes[n];
+  F = StreamPass{};
+  F.op = SP_COPY;
+  F.nl = uint32_t(lanes_of(kind));
+  F.chunks = pts * B * F.nl / 4;
+  F.plane_chunks = plane_div(F.nl);
+  F.row_chunks = make_fastdiv(W / 4);
+  F.width = W;
+  F.vbytes = bpe(kind) / F.nl;
+  if (!(wid == FK_OP_SPLIT_WRITE && kind == FK_F32X3) && !(wid == FK_OP_PER_THREAD_WRITE && F.nl == 1)) return;
+  if (lane_kind(kind) != FK_F32 && kind != FK_U8) return;
+  const uint64_t align = F.vbytes == 4 ? 16 : 4;
+  for (const DWrite& w : writes)
+    for (uint32_t l = 0; l < F.nl; ++l)
+      if ((w.flags & WF_ACTIVE) && ((w.dst[l] | w.pitch[l]) % align)) return;
+  F.wr = writes[0];  // non-batch; a BatchWrite's table (dp.d_writes) is set at launch
+  // pass 0
+  const DSample& s0 = dp.reads[0];
+  bool direct = uint32_t(p.read.out_kind) == FK_F32;
+  for (uint32_t z = 0; z < B && direct; ++z) {
+    const DSample& s = dp.reads[z];
+    direct = !(s.flags & SF_DEFAULT) && s.mode == RD_DIRECT && s.kind == FK_F32 && s.post_len == 0 && s.x0 == 0 &&
+             s.y0 == 0 && s.pitch == uint64_t(W) * 4 && s.src == s0.src + uint64_t(z) * pts * 4 && s.src % 16 == 0;
+  }
+  if (!direct) {  // fk_walk over op 0 into the planar intermediate [z][lane][H W]
+    if (!dp.affine_ok || uint32_t(p.compute[0].out_kind) != FK_F32X3) return;
+    std::vector<DOp> one{ops[0]};
+    if (ops[0].cls != OC_ARITH || ops[0].repeat != 1) return;
+    uint32_t fast = ops[0].fn == AF_DIV && recip_div_exact(one, 0, dp.per_z_host, B) ? 1u : 0u;
+    const uint32_t sig = sig_make(1, ops[0].fn, 0, 0, 0, fast);
+    std::vector<DWrite> planar(B);
+    for (uint32_t z = 0; z < B; ++z) {
+      planar[z] = DWrite{};
+      for (int l = 0; l < 3; ++l) {
+        planar[z].dst[l] = (uint64_t(z) * 3 + l) * pts * 4;  // offsets: WalkPlan::dst_base adds the buffer
+        planar[z].pitch[l] = uint64_t(W) * 4;
+      }
+      planar[z].flags = WF_ACTIVE;
+    }
+    if (!build_walk(dp, p, one, sig, planar, dp.unf_walk_plan, dp.unf_walk_sig, dp.unf_walk_perz)) return;
+    dp.unf_walk = true;
+  }
+  dp.unf_pass = passes;
+  dp.unf_bytes = bytes;
+  dp.unf_fast = true;
 }
 
 bool sep_stage_ok(const DeviceProgram& dp, uint32_t W, uint32_t T, uint32_t spc);
@@ -772,7 +874,8 @@ std::shared_ptr<DeviceProgram> build_program(const Pipeline& p, int device) {
         }
       }
     }
-    build_walk(*dp, p, arith, sig, writes);
+    dp->walk_ok = build_walk(*dp, p, arith, sig, writes, dp->walk, dp->walk_sig, dp->walk_perz);
+    build_unfused(*dp, p, writes);
   }
   // direct f32 kernel: f32 planes read as-is, f32 arith runs (any repeat), an
   // optional final Cast f32 -> u8, a packed write
@@ -1144,6 +1247,42 @@ fk_exec_report execute_unfused(const Pipeline& p, const fk_exec_config* cfg) {
   Timer timer(st, cfg && (cfg->flags & FK_EXEC_TIMED));
   const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
   const size_t n = p.compute.size();
+  if (dp.unf_fast && !(cfg && (cfg->flags & FK_EXEC_FORCE_GENERIC))) {
+    // one compiled streaming pass per op (planar intermediates), then the write pass
+    void* prev = nullptr;
+    for (size_t i = 0; i <= n; ++i) {
+      void* next = nullptr;
+      if (i < n) {
+        cuda_check(cudaMallocAsync(&next, dp.unf_bytes[i], st), "cudaMallocAsync(intermediate)");
+        r.intermediate_bytes_allocated += dp.unf_bytes[i];
+      }
+      if (i == 0 && dp.unf_walk) {
+        WalkPlan C = dp.unf_walk_plan;
+        C.reads = dp.d_reads;
+        C.dst_base = reinterpret_cast<uint64_t>(next);
+        cuda_check(launch_walk(dp.unf_walk_sig, dp.unf_walk_perz, C, st), "fk_walk launch (unfused pass 0)");
+      } else {
+        StreamPass S = dp.unf_pass[i];
+        S.src = static_cast<const uint8_t*>(i == 0 ? reinterpret_cast<void*>(dp.reads[0].src) : prev);
+        S.dst = static_cast<uint8_t*>(next);
+        if (i == n && p.write.id == FK_OP_BATCH_WRITE) S.writes = dp.d_writes;
+        cuda_check(launch_stream(S, st), "fk_stream launch");
+      }
+      ++r.kernels_launched;
+      g_launches.fetch_add(1, std::memory_order_relaxed);
+      if (prev) cuda_check(cudaFreeAsync(prev, st), "cudaFreeAsync(intermediate)");
+      prev = next;
+    }
+    t_last_kernel = "fk_stream";
+    r.device_ms = timer.stop();
+    r.wall_time_ns = now_ns() - t0;
+    r.bytes_read = dp.traffic.unfused_read;
+    r.bytes_written = dp.traffic.unfused_written;
+    r.passes = n + 1;
+    r.points_visited = uint64_t(W) * H * B * r.passes;
+    r.path = FK_PATH_COMPILED;
+    return r;
+  }
   if (n == 0) {  // executor.cpp:144-166: one read -> write sweep
     const int cls = generic_state_class(dp.fused_wide, dp.fused_lanes);
     DPlan P = base_plan(W, H, B, dp.read_flat && dp.write_flat, generic_elems(cls));

@@ -186,7 +186,7 @@ __device__ __noinline__ void fix_pair(const WalkPlan& P, uint32_t z, uint32_t x,
           default: v = __fdiv_rn(v, cst); break;
         }
       }
-      __stcs(reinterpret_cast<float*>(A.dst[m] + uint64_t(y) * A.dpitch) + x + c, v);
+      __stcs(reinterpret_cast<float*>(P.dst_base + A.dst[m] + uint64_t(y) * A.dpitch) + x + c, v);
     }
   }
 }
@@ -338,7 +338,7 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   const uint64_t kR = p2::pack(kRound, kRound);
   uint64_t dst[3];
 #pragma unroll
-  for (int m = 0; m < 3; ++m) dst[m] = A.dst[m] + 4ull * x;
+  for (int m = 0; m < 3; ++m) dst[m] = P.dst_base + A.dst[m] + 4ull * x;
   const uint32_t dpitch = A.dpitch;
   using KS = typename std::conditional<PERZ, KReg<SIG>, KInl<SIG>>::type;
   const KS ks = [&]() {

@@ -95,6 +95,7 @@ struct WalkPlan {
   uint32_t max_rows;        // output rows of the largest unit (fix-mask capacity)
   uint32_t elem;            // tensor-map element bytes (2, 4 or 8)
   uint64_t negz;            // kNegZero2 (fk_pack2.cuh): a product's runtime -0 addend
+  uint64_t dst_base;        // added to every WalkAux::dst (0: absolute; the unfused pass 0: its intermediate)
   // inline chain constants (shared by every plane), input-lane order, as pairs
   float2 kc[4][3], kh[4][3], kl[4][3];
 };
