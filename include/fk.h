@@ -137,6 +137,11 @@ fk_status fk_plane_view(const fk_plane* p, uint32_t x0, uint32_t y0, uint32_t w,
  * CUDA backend: device memory on the current device; CPU backends: host memory. */
 fk_status fk_plane_alloc(uint32_t width, uint32_t height, uint32_t kind, uint32_t row_stride, fk_plane* out);
 void fk_plane_free(fk_plane* p);
+/* Host <-> plane copies for bindings without a CUDA runtime: the plane's
+ * width x height elements row by row, host rows host_pitch bytes apart
+ * (0 = packed). CUDA backend: synchronous cudaMemcpy2D; CPU backends: memcpy. */
+fk_status fk_plane_upload(const fk_plane* dst, const void* host, size_t host_pitch);
+fk_status fk_plane_download(const fk_plane* src, void* host, size_t host_pitch);
 uint32_t fk_bytes_per_element(uint32_t kind);                    /* scalar.hpp:27-37 */
 
 /* ---- IOp builders (oplib.hpp:31-76) -------------------------------------- */

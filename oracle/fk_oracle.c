@@ -272,6 +272,25 @@ void fk_plane_free(fk_plane* p) {
   }
 }
 
+static fk_status plane_copy(const fk_plane* p, void* host, size_t host_pitch, int up) {
+  if (!plane_ok(p) || !host) return fail(FK_E_INVALID_ARGUMENT, -1, "InvalidArgument: bad plane copy");
+  size_t row = (size_t)p->width * fk_bytes_per_element(p->kind);
+  size_t hp = host_pitch ? host_pitch : row, pp = (size_t)p->row_stride * fk_bytes_per_element(p->kind);
+  for (uint32_t y = 0; y < p->height; ++y) {
+    uint8_t* dev = (uint8_t*)p->data + y * pp;
+    uint8_t* h = (uint8_t*)host + y * hp;
+    if (up) memcpy(dev, h, row);
+    else memcpy(h, dev, row);
+  }
+  return FK_OK;
+}
+fk_status fk_plane_upload(const fk_plane* dst, const void* host, size_t host_pitch) {
+  return plane_copy(dst, (void*)host, host_pitch, 1);
+}
+fk_status fk_plane_download(const fk_plane* src, void* host, size_t host_pitch) {
+  return plane_copy(src, host, host_pitch, 0);
+}
+
 static int sample_resizing(const sample_t* s) { return s->out_w != s->rect_w || s->out_h != s->rect_h; }
 static uint32_t sample_out_kind(const sample_t* s) { /* ops.hpp:88-90 */
   return s->n_post ? s->post[s->n_post - 1].out : s->source.kind;

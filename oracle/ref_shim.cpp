@@ -203,6 +203,25 @@ void fk_plane_free(fk_plane* p) {
   }
 }
 
+static fk_status plane_copy(const fk_plane* p, void* host, size_t host_pitch, bool up) {
+  if (!plane_ok(p) || !host) return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: bad plane copy");
+  const size_t row = size_t(p->width) * fk_bytes_per_element(p->kind);
+  const size_t hp = host_pitch ? host_pitch : row, pp = size_t(p->row_stride) * fk_bytes_per_element(p->kind);
+  for (uint32_t y = 0; y < p->height; ++y) {
+    uint8_t* d = static_cast<uint8_t*>(p->data) + y * pp;
+    uint8_t* h = static_cast<uint8_t*>(host) + y * hp;
+    if (up) std::memcpy(d, h, row);
+    else std::memcpy(h, d, row);
+  }
+  return FK_OK;
+}
+fk_status fk_plane_upload(const fk_plane* dst, const void* host, size_t host_pitch) {
+  return plane_copy(dst, const_cast<void*>(host), host_pitch, true);
+}
+fk_status fk_plane_download(const fk_plane* src, void* host, size_t host_pitch) {
+  return plane_copy(src, host, host_pitch, false);
+}
+
 fk_status fk_op_arith(uint32_t op_id, uint32_t kind, const void* value, fk_iop** out) {
   if (op_id < FK_OP_MUL || op_id > FK_OP_DIV || kind > FK_F64X3 || !value)
     return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: bad arith op");

@@ -112,6 +112,8 @@ SIGNATURES = {
     "fk_bytes_per_element": (U32, [U32]),
     "fk_plane_alloc": (I32, [U32, U32, U32, U32, C.POINTER(fk_plane)]),
     "fk_plane_free": (None, [C.POINTER(fk_plane)]),
+    "fk_plane_upload": (I32, [C.POINTER(fk_plane), P, C.c_size_t]),
+    "fk_plane_download": (I32, [C.POINTER(fk_plane), P, C.c_size_t]),
     "fk_op_arith": (I32, [U32, U32, P, PP]),
     "fk_op_cast": (I32, [U32, U32, PP]),
     "fk_op_static_loop": (I32, [P, U32, PP]),

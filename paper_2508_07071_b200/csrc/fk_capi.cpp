@@ -180,6 +180,27 @@ void fk_plane_free(fk_plane* pl) {
   pl->data = nullptr;
 }
 
+fk_status fk_plane_upload(const fk_plane* dst, const void* host, size_t host_pitch) {
+  return guard([&] {
+    fk::check_plane(dst, "destination");
+    if (!host) fk::fail(FK_E_INVALID_ARGUMENT, "null host buffer");
+    const size_t row = size_t(dst->width) * fk::bpe(dst->kind);
+    cuda_ok(cudaMemcpy2D(dst->data, size_t(dst->row_stride) * fk::bpe(dst->kind), host, host_pitch ? host_pitch : row,
+                         row, dst->height, cudaMemcpyDefault),
+            "plane upload");
+  });
+}
+fk_status fk_plane_download(const fk_plane* src, void* host, size_t host_pitch) {
+  return guard([&] {
+    fk::check_plane(src, "source");
+    if (!host) fk::fail(FK_E_INVALID_ARGUMENT, "null host buffer");
+    const size_t row = size_t(src->width) * fk::bpe(src->kind);
+    cuda_ok(cudaMemcpy2D(host, host_pitch ? host_pitch : row, src->data, size_t(src->row_stride) * fk::bpe(src->kind),
+                         row, src->height, cudaMemcpyDefault),
+            "plane download");
+  });
+}
+
 fk_status fk_op_arith(uint32_t id, uint32_t kind, const void* value, fk_iop** out) {
   return build(out, [&] { return fk::make_arith(id, kind, value); });
 }
