@@ -188,6 +188,18 @@ fk_status fk_plan_memory_savings(const fk_pipeline* p, uint64_t* bytes);        
 fk_status fk_schedule(const fk_extent3* space, const fk_exec_config* cfg, uint32_t* tasks,
                       uint64_t cap, uint64_t* count);
 
+/* ---- FKT tensor files (tensor_io.hpp:13-18, tensor_io.cpp:12-117) --
+ * Little-endian "FKT1" | u32 plane_count | per plane: u32 kind_tag | u32 width |
+ * u32 height | width*height elements row-major. Planes of one file share a kind
+ * (PlaneBatch, plane.cpp:149-161). Errors as the reference: IoError, BadMagic,
+ * TruncatedPayload, EmptyBatch, UnknownKindTag, InnerKindMismatch.
+ * fk_tensor_read_file: *count = planes in the file; when cap >= *count the
+ * planes are allocated with fk_plane_alloc (device memory with the CUDA
+ * backend; release each with fk_plane_free) and written to out[0..count). */
+fk_status fk_tensor_write_file(const fk_plane* planes, uint32_t n, const char* path);
+fk_status fk_tensor_read_file(const char* path, fk_plane* out, uint32_t cap, uint32_t* count);
+fk_status fk_write_ppm(const fk_plane* plane, const char* path);  /* P6 export of a u8x3 plane */
+
 /* ---- multi-GPU batch sharding ----------------------------
  * The reference partitions a batch z-major into independent tasks
  * (executor.cpp:52-61, ops.cpp:369-378); across GPUs each device runs the

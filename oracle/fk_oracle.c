@@ -291,6 +291,84 @@ fk_status fk_plane_download(const fk_plane* src, void* host, size_t host_pitch) 
   return plane_copy(src, host, host_pitch, 0);
 }
 
+/* ---- FKT files: tensor_io.cpp:12-117 restated (little-endian host) ---- */
+static int put_u32(FILE* f, uint32_t v) {
+  unsigned char b[4] = {(unsigned char)v, (unsigned char)(v >> 8), (unsigned char)(v >> 16), (unsigned char)(v >> 24)};
+  return fwrite(b, 1, 4, f) == 4;
+}
+static int get_u32(FILE* f, uint32_t* v) {
+  unsigned char b[4];
+  if (fread(b, 1, 4, f) != 4) return 0;
+  *v = (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) | ((uint32_t)b[3] << 24);
+  return 1;
+}
+fk_status fk_tensor_write_file(const fk_plane* planes, uint32_t n, const char* path) {
+  if (!path) return fail(FK_E_INVALID_ARGUMENT, -1, "InvalidArgument: null path");
+  if (n == 0 || !planes) return fail(FK_E_EMPTY_BATCH, -1, "EmptyBatch: plane batch must be non-empty");
+  for (uint32_t i = 0; i < n; ++i) {
+    if (!plane_ok(&planes[i])) return fail(FK_E_INVALID_ARGUMENT, -1, "InvalidArgument: invalid plane");
+    if (planes[i].kind != planes[0].kind)
+      return fail(FK_E_INNER_KIND_MISMATCH, -1, "InnerKindMismatch: mixed element kinds in one batch");
+  }
+  FILE* f = fopen(path, "wb");
+  if (!f) return fail(FK_E_IO_ERROR, -1, "IoError: cannot open for writing: %s", path);
+  int ok = fwrite("FKT1", 1, 4, f) == 4 && put_u32(f, n);
+  for (uint32_t i = 0; i < n && ok; ++i) {
+    const fk_plane* p = &planes[i];
+    size_t row = (size_t)p->width * fk_bytes_per_element(p->kind);
+    ok = put_u32(f, p->kind) && put_u32(f, p->width) && put_u32(f, p->height);
+    for (uint32_t y = 0; y < p->height && ok; ++y)
+      ok = fwrite((const uint8_t*)p->data + (size_t)y * p->row_stride * fk_bytes_per_element(p->kind), 1, row, f) == row;
+  }
+  fclose(f);
+  return ok ? FK_OK : fail(FK_E_IO_ERROR, -1, "IoError: write failed: %s", path);
+}
+fk_status fk_tensor_read_file(const char* path, fk_plane* out, uint32_t cap, uint32_t* count) {
+  if (!path || !count) return fail(FK_E_INVALID_ARGUMENT, -1, "InvalidArgument: null argument");
+  FILE* f = fopen(path, "rb");
+  if (!f) return fail(FK_E_IO_ERROR, -1, "IoError: cannot open for reading: %s", path);
+  char magic[4];
+  uint32_t n = 0;
+  fk_status st = FK_OK;
+  if (fread(magic, 1, 4, f) != 4) st = fail(FK_E_TRUNCATED_PAYLOAD, -1, "TruncatedPayload: file shorter than magic");
+  else if (memcmp(magic, "FKT1", 4) != 0) st = fail(FK_E_BAD_MAGIC, -1, "BadMagic: %s", path);
+  else if (!get_u32(f, &n)) st = fail(FK_E_TRUNCATED_PAYLOAD, -1, "TruncatedPayload: unexpected end of file in header");
+  else if (n == 0) st = fail(FK_E_EMPTY_BATCH, -1, "EmptyBatch: file declares zero planes");
+  if (st != FK_OK) { fclose(f); return st; }
+  *count = n;
+  if (cap < n || !out) { fclose(f); return FK_OK; }
+  uint32_t got = 0;
+  for (; got < n && st == FK_OK; ++got) {
+    uint32_t tag, w, h;
+    if (!get_u32(f, &tag)) { st = fail(FK_E_TRUNCATED_PAYLOAD, -1, "TruncatedPayload: unexpected end of file in header"); break; }
+    if (tag > FK_F64X3) { st = fail(FK_E_UNKNOWN_KIND_TAG, -1, "UnknownKindTag: kind tag %u", tag); break; }
+    if (!get_u32(f, &w) || !get_u32(f, &h)) { st = fail(FK_E_TRUNCATED_PAYLOAD, -1, "TruncatedPayload: unexpected end of file in header"); break; }
+    if (got > 0 && tag != out[0].kind) { st = fail(FK_E_INNER_KIND_MISMATCH, -1, "InnerKindMismatch: mixed element kinds in one batch"); break; }
+    if ((st = fk_plane_alloc(w, h, tag, 0, &out[got])) != FK_OK) break;
+    size_t bytes = (size_t)w * h * fk_bytes_per_element(tag);
+    if (fread(out[got].data, 1, bytes, f) != bytes) {
+      fk_plane_free(&out[got]);
+      st = fail(FK_E_TRUNCATED_PAYLOAD, -1, "TruncatedPayload: plane %u payload", got);
+      break;
+    }
+  }
+  fclose(f);
+  if (st != FK_OK)
+    for (uint32_t i = 0; i < got; ++i) fk_plane_free(&out[i]);
+  return st;
+}
+fk_status fk_write_ppm(const fk_plane* p, const char* path) {
+  if (!plane_ok(p) || !path) return fail(FK_E_INVALID_ARGUMENT, -1, "InvalidArgument: bad arguments");
+  if (p->kind != FK_U8X3) return fail(FK_E_UNSUPPORTED_KIND, -1, "UnsupportedKind: PPM export needs a u8x3 plane");
+  FILE* f = fopen(path, "wb");
+  if (!f) return fail(FK_E_IO_ERROR, -1, "IoError: cannot open for writing: %s", path);
+  int ok = fprintf(f, "P6\n%u %u\n255\n", p->width, p->height) > 0;
+  for (uint32_t y = 0; y < p->height && ok; ++y)
+    ok = fwrite((const uint8_t*)p->data + (size_t)y * p->row_stride * 3, 1, (size_t)p->width * 3, f) == (size_t)p->width * 3;
+  fclose(f);
+  return ok ? FK_OK : fail(FK_E_IO_ERROR, -1, "IoError: write failed: %s", path);
+}
+
 static int sample_resizing(const sample_t* s) { return s->out_w != s->rect_w || s->out_h != s->rect_h; }
 static uint32_t sample_out_kind(const sample_t* s) { /* ops.hpp:88-90 */
   return s->n_post ? s->post[s->n_post - 1].out : s->source.kind;

@@ -26,6 +26,7 @@
 #include "opfuse/dpp.hpp"
 #include "opfuse/executor.hpp"
 #include "opfuse/oplib.hpp"
+#include "opfuse/tensor_io.hpp"
 #include "opfuse/ops.hpp"
 #include "fk.h"
 
@@ -220,6 +221,56 @@ fk_status fk_plane_upload(const fk_plane* dst, const void* host, size_t host_pit
 }
 fk_status fk_plane_download(const fk_plane* src, void* host, size_t host_pitch) {
   return plane_copy(src, host, host_pitch, false);
+}
+
+// FKT files through the reference's own tensor_io (tensor_io.cpp:12-117)
+static Plane host_copy(const fk_plane& p) {
+  Plane q = Plane::alloc(p.width, p.height, static_cast<ScalarKind>(p.kind));
+  const size_t row = size_t(p.width) * fk_bytes_per_element(p.kind);
+  for (uint32_t y = 0; y < p.height; ++y)
+    std::memcpy(q.row_mut(y), static_cast<const uint8_t*>(p.data) + size_t(y) * p.row_stride * fk_bytes_per_element(p.kind), row);
+  return q;
+}
+fk_status fk_tensor_write_file(const fk_plane* planes, uint32_t n, const char* path) {
+  if (!path) return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: null path");
+  try {
+    std::vector<Plane> v;
+    for (uint32_t i = 0; planes && i < n; ++i) {
+      if (!plane_ok(&planes[i])) return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: invalid plane");
+      v.push_back(host_copy(planes[i]));
+    }
+    tensor_write_file(PlaneBatch(std::move(v)), path);
+    return FK_OK;
+  } catch (const Error& e) {
+    return set_error(e);
+  }
+}
+fk_status fk_tensor_read_file(const char* path, fk_plane* out, uint32_t cap, uint32_t* count) {
+  if (!path || !count) return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: null argument");
+  try {
+    const PlaneBatch b = tensor_read_file(path);
+    *count = uint32_t(b.size());
+    if (cap < b.size() || !out) return FK_OK;
+    for (size_t i = 0; i < b.size(); ++i) {
+      const Plane& p = b[i];
+      fk_plane_alloc(p.width(), p.height(), uint32_t(p.kind()), 0, &out[i]);
+      const size_t row = size_t(p.width()) * bytes_per_element(p.kind());
+      for (uint32_t y = 0; y < p.height(); ++y)
+        std::memcpy(static_cast<uint8_t*>(out[i].data) + y * row, p.row(y), row);
+    }
+    return FK_OK;
+  } catch (const Error& e) {
+    return set_error(e);
+  }
+}
+fk_status fk_write_ppm(const fk_plane* p, const char* path) {
+  if (!plane_ok(p) || !path) return set_error(FK_E_INVALID_ARGUMENT, "InvalidArgument: bad arguments");
+  try {
+    write_ppm(host_copy(*p), path);
+    return FK_OK;
+  } catch (const Error& e) {
+    return set_error(e);
+  }
 }
 
 fk_status fk_op_arith(uint32_t op_id, uint32_t kind, const void* value, fk_iop** out) {

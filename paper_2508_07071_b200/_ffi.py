@@ -143,6 +143,9 @@ SIGNATURES = {
     "fk_schedule": (I32, [C.POINTER(fk_extent3), C.POINTER(fk_exec_config), C.POINTER(C.c_uint32),
                           C.c_uint64, C.POINTER(C.c_uint64)]),
     "fk_multi_reduce_plane": (I32, [P, C.POINTER(fk_reduce_spec), U32, I32, P, C.POINTER(C.c_uint64)]),
+    "fk_tensor_write_file": (I32, [C.POINTER(fk_plane), U32, C.c_char_p]),
+    "fk_tensor_read_file": (I32, [C.c_char_p, C.POINTER(fk_plane), U32, C.POINTER(U32)]),
+    "fk_write_ppm": (I32, [C.POINTER(fk_plane), C.c_char_p]),
     "fk_execute_sharded": (I32, [PP, C.POINTER(I32), U32, C.POINTER(fk_exec_config), C.POINTER(fk_exec_report)]),
     "fk_gather": (I32, [P, I32, C.POINTER(C.c_uint64), PP, C.POINTER(I32), C.POINTER(C.c_uint64), U32, P]),
 }

@@ -33,8 +33,9 @@ class LazyHandle:
     """A deferred operation (api.hpp:13-32): constructing one executes nothing."""
     provenance: str
     uid: int
-    iop: IOp | None = None          # None: deferred cvt_color
+    iop: IOp | None = None          # None: deferred cvt_color / cast
     color_order: int = 0
+    cast_to: int | None = None      # deferred cast: the target kind
     lib: Library | None = field(default=None, compare=False)
 
     @property
@@ -81,6 +82,13 @@ def cvt_color(order: int) -> LazyHandle:
     return LazyHandle("cvt_color", next(_uids), None, order)
 
 
+def cast(to: int) -> LazyHandle:
+    """The handle the reference facade lacks: cast the flowing
+    value to kind `to`; the source kind is taken from the chain when the pipeline
+    is built (like cvt_color)."""
+    return LazyHandle("cast", next(_uids), None, 0, to)
+
+
 def multiply(c: Const, lib: Library | None = None) -> LazyHandle:
     return _handle("multiply", lambda L: L.op_mul(c), lib)
 
@@ -112,8 +120,11 @@ def _resolve_chain(handles: Sequence[LazyHandle], lib: Library) -> list[IOp]:
     for i, h in enumerate(handles):
         if h.deferred:
             if current is None:
-                raise OpfuseError(1 + 3, "KindMismatch: cvt_color has no upstream value", i, h.provenance)
-            op = _guarded(h.provenance, lambda: lib.op_color_convert(h.color_order, current))
+                raise OpfuseError(1 + 3, f"KindMismatch: {h.provenance} has no upstream value", i, h.provenance)
+            if h.cast_to is not None:
+                op = _guarded(h.provenance, lambda: lib.op_cast(current, h.cast_to))
+            else:
+                op = _guarded(h.provenance, lambda: lib.op_color_convert(h.color_order, current))
             current = op.output_kind
             ops.append(op)
         else:

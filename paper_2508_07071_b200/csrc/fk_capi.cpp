@@ -3,6 +3,8 @@
 // leaves the message / chain position in thread-local storage.
 #include <cuda_runtime.h>
 
+#include <cstdio>
+
 #include <cstring>
 #include <map>
 #include <memory>
@@ -70,6 +72,11 @@ Holds holds_of(const fk::Op& op) {
 
 thread_local std::string g_err;
 thread_local int32_t g_pos = -1;
+
+// an fk_* call inside another entry point: rethrow its failure unchanged
+void check_status(fk_status s) {
+  if (s != FK_OK) throw fk::Error(s, g_err, g_pos);
+}
 
 template <class Fn>
 fk_status guard(Fn&& fn) {
@@ -311,6 +318,106 @@ fk_status fk_execute_fused(const fk_pipeline* p, const fk_exec_config* cfg, fk_e
     if (rep) *rep = r;
   });
 }
+namespace {
+// FKT little-endian u32 fields (tensor_io.cpp:16-29); this library only runs on little-endian hosts
+void put_u32(std::FILE* f, uint32_t v) {
+  const unsigned char b[4] = {uint8_t(v), uint8_t(v >> 8), uint8_t(v >> 16), uint8_t(v >> 24)};
+  if (std::fwrite(b, 1, 4, f) != 4) fk::fail(FK_E_IO_ERROR, "write failed");
+}
+uint32_t get_u32(std::FILE* f) {
+  unsigned char b[4];
+  if (std::fread(b, 1, 4, f) != 4) fk::fail(FK_E_TRUNCATED_PAYLOAD, "unexpected end of file in header");
+  return uint32_t(b[0]) | (uint32_t(b[1]) << 8) | (uint32_t(b[2]) << 16) | (uint32_t(b[3]) << 24);
+}
+struct File {
+  std::FILE* f;
+  ~File() {
+    if (f) std::fclose(f);
+  }
+};
+}  // namespace
+
+fk_status fk_tensor_write_file(const fk_plane* planes, uint32_t n, const char* path) {
+  return guard([&] {  // tensor_io.cpp:61-83
+    if (!path) fk::fail(FK_E_INVALID_ARGUMENT, "null path");
+    if (n == 0 || !planes) fk::fail(FK_E_EMPTY_BATCH, "plane batch must be non-empty");
+    for (uint32_t i = 0; i < n; ++i) {
+      fk::check_plane(&planes[i], "plane");
+      if (planes[i].kind != planes[0].kind) fk::fail(FK_E_INNER_KIND_MISMATCH, "mixed element kinds in one batch");
+    }
+    File out{std::fopen(path, "wb")};
+    if (!out.f) fk::fail(FK_E_IO_ERROR, std::string("cannot open for writing: ") + path);
+    if (std::fwrite("FKT1", 1, 4, out.f) != 4) fk::fail(FK_E_IO_ERROR, "write failed");
+    put_u32(out.f, n);
+    std::vector<uint8_t> host;
+    for (uint32_t i = 0; i < n; ++i) {
+      const fk_plane& p = planes[i];
+      put_u32(out.f, p.kind);
+      put_u32(out.f, p.width);
+      put_u32(out.f, p.height);
+      host.resize(size_t(p.width) * p.height * fk::bpe(p.kind));
+      check_status(fk_plane_download(&p, host.data(), 0));
+      if (std::fwrite(host.data(), 1, host.size(), out.f) != host.size())
+        fk::fail(FK_E_IO_ERROR, std::string("write failed: ") + path);
+    }
+  });
+}
+
+fk_status fk_tensor_read_file(const char* path, fk_plane* out, uint32_t cap, uint32_t* count) {
+  return guard([&] {  // tensor_io.cpp:85-109
+    if (!path || !count) fk::fail(FK_E_INVALID_ARGUMENT, "null argument");
+    File in{std::fopen(path, "rb")};
+    if (!in.f) fk::fail(FK_E_IO_ERROR, std::string("cannot open for reading: ") + path);
+    char magic[4];
+    if (std::fread(magic, 1, 4, in.f) != 4) fk::fail(FK_E_TRUNCATED_PAYLOAD, "file shorter than magic");
+    if (std::memcmp(magic, "FKT1", 4) != 0) fk::fail(FK_E_BAD_MAGIC, std::string("") + path);
+    const uint32_t n = get_u32(in.f);
+    if (n == 0) fk::fail(FK_E_EMPTY_BATCH, "file declares zero planes");
+    *count = n;
+    if (cap < n || !out) return;
+    std::vector<fk_plane> got;
+    struct Undo {  // release what was allocated when a later plane fails
+      std::vector<fk_plane>& v;
+      bool done = false;
+      ~Undo() {
+        if (!done)
+          for (fk_plane& p : v) fk_plane_free(&p);
+      }
+    } undo{got};
+    std::vector<uint8_t> host;
+    for (uint32_t i = 0; i < n; ++i) {
+      const uint32_t tag = get_u32(in.f);
+      if (tag > FK_F64X3) fk::fail(FK_E_UNKNOWN_KIND_TAG, "kind tag " + std::to_string(tag));
+      const uint32_t w = get_u32(in.f), h = get_u32(in.f);
+      if (!got.empty() && tag != got[0].kind) fk::fail(FK_E_INNER_KIND_MISMATCH, "mixed element kinds in one batch");
+      host.resize(size_t(w) * h * fk::bpe(tag));
+      if (std::fread(host.data(), 1, host.size(), in.f) != host.size())
+        fk::fail(FK_E_TRUNCATED_PAYLOAD, "plane " + std::to_string(i) + " payload");
+      fk_plane p{};
+      check_status(fk_plane_alloc(w, h, tag, 0, &p));
+      got.push_back(p);
+      check_status(fk_plane_upload(&p, host.data(), 0));
+    }
+    for (uint32_t i = 0; i < n; ++i) out[i] = got[i];
+    undo.done = true;
+  });
+}
+
+fk_status fk_write_ppm(const fk_plane* plane, const char* path) {
+  return guard([&] {  // tensor_io.cpp:111-124
+    fk::check_plane(plane, "plane");
+    if (!path) fk::fail(FK_E_INVALID_ARGUMENT, "null path");
+    if (plane->kind != FK_U8X3) fk::fail(FK_E_UNSUPPORTED_KIND, "PPM export needs a u8x3 plane");
+    std::vector<uint8_t> host(size_t(plane->width) * plane->height * 3);
+    check_status(fk_plane_download(plane, host.data(), 0));
+    File out{std::fopen(path, "wb")};
+    if (!out.f) fk::fail(FK_E_IO_ERROR, std::string("cannot open for writing: ") + path);
+    std::fprintf(out.f, "P6\n%u %u\n255\n", plane->width, plane->height);
+    if (std::fwrite(host.data(), 1, host.size(), out.f) != host.size())
+      fk::fail(FK_E_IO_ERROR, std::string("write failed: ") + path);
+  });
+}
+
 fk_status fk_execute_sharded(const fk_pipeline* const* pipelines, const int32_t* devices, uint32_t n,
                              const fk_exec_config* cfgs, fk_exec_report* reports) {
   return guard([&] {

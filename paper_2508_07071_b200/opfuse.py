@@ -457,6 +457,38 @@ class Library:
     def execute_unfused(self, pipeline, cfg: ExecConfig | None = None) -> ExecReport:
         return self._exec(self._c.fk_execute_unfused, pipeline, cfg)
 
+    # -- FKT tensor files (tensor_io.hpp:13-18)
+    def tensor_write_file(self, planes, path: str):
+        """tensor_write_file: planes (Plane / SharedPlane / RawPlane, one kind) -> an FKT1 file."""
+        arr = (_ffi.fk_plane * max(len(planes), 1))(*(p.c() for p in planes))
+        self._check(self._c.fk_tensor_write_file(arr, len(planes), str(path).encode()))
+
+    def tensor_read_file(self, path: str) -> list:
+        """tensor_read_file: the file's planes as library-owned SharedPlanes."""
+        n = C.c_uint32()
+        self._check(self._c.fk_tensor_read_file(str(path).encode(), None, 0, C.byref(n)))
+        arr = (_ffi.fk_plane * max(n.value, 1))()
+        self._check(self._c.fk_tensor_read_file(str(path).encode(), arr, n.value, C.byref(n)))
+        return [SharedPlane(self, _ffi.fk_plane(arr[i].data, arr[i].width, arr[i].height, arr[i].row_stride,
+                                                arr[i].kind)) for i in range(n.value)]
+
+    def write_ppm(self, plane, path: str):
+        self._check(self._c.fk_write_ppm(C.byref(plane.c()), str(path).encode()))
+
+    def download(self, plane) -> np.ndarray:
+        """A plane's elements as a packed host array (fk_plane_download)."""
+        c = plane.c()
+        bpe = BYTES_PER_ELEMENT[c.kind]
+        buf = np.empty(c.width * c.height * bpe, np.uint8)
+        self._check(self._c.fk_plane_download(C.byref(c), buf.ctypes.data, 0))
+        arr = buf.view(_NP_DTYPE[c.kind])
+        return arr.reshape(c.height, c.width, 3) if LANES[c.kind] == 3 else arr.reshape(c.height, c.width)
+
+    def upload(self, plane, arr: np.ndarray):
+        c = plane.c()
+        a = np.ascontiguousarray(arr)
+        self._check(self._c.fk_plane_upload(C.byref(c), a.ctypes.data, 0))
+
     def execute_sharded(self, pipelines, devices, cfgs=None):
         """fk_execute_sharded: pipelines[i] (a batch shard) on devices[i], all enqueued
         before any wait; returns one ExecReport per shard."""

@@ -84,3 +84,31 @@ def test_execute_batch_heterogeneous_counts(lib):
     with pytest.raises(OpfuseError) as e:
         api.execute_batch([api.read(a, lib=lib)], [], [])
     assert e.value.code == "HeterogeneousBatch"
+
+
+def test_cast_handle(lib):
+    """The facade's cast handle (absent from the reference api.hpp):
+    u8x3 frame -> cvt -> cast f32x3 -> subtract, built from handles only."""
+    if lib.name.startswith("reference"):
+        pytest.skip("the reference facade has no cast handle; checked on the oracle")
+    rng = np.random.default_rng(3)
+    frame = lib.plane_from_numpy(rng.integers(0, 256, (20, 30, 3), dtype=np.uint8))
+    out = [lib.plane_alloc(10, 8, F32) for _ in range(3)]
+    handles = [api.resize(api.crop(frame, 2, 3, 20, 16, lib=lib), 10, 8, BILINEAR, lib=lib),
+               api.cvt_color(SWAP_RB), api.cast(F32X3), api.subtract(f32x3(1, 2, 3), lib=lib),
+               api.split(out, lib=lib)]
+    p = api.build_pipeline(handles)
+    assert p.n_compute == 1       # swap and cast folded into the read
+    api.execute_operations(handles)
+    ref = Library("oracle")
+    want = [ref.plane_alloc(10, 8, F32) for _ in range(3)]
+    src = ref.plane_from_numpy(frame.to_numpy())
+    rd = ref.fold_unary_into_read(ref.fold_unary_into_read(
+        ref.op_resize(ref.op_crop(src, 2, 3, 20, 16), 10, 8, BILINEAR), ref.op_color_convert(SWAP_RB, U8X3)),
+        ref.op_cast(U8X3, F32X3))
+    ref.execute_fused(ref.validate_chain([rd, ref.op_sub(f32x3(1, 2, 3)), ref.op_split_write(want)]))
+    for a, b in zip(out, want):
+        assert np.array_equal(a.to_numpy(), b.to_numpy())
+    with pytest.raises(OpfuseError) as e:
+        api.build_pipeline([api.cast(F32), api.write(out[0], lib=lib)])
+    assert e.value.provenance == "cast"
