@@ -255,6 +255,18 @@ def sub_result(lib, cfg, stream, flush, workload, n_ops=64, crops=8192, steps=10
         lib.execute_fused(pipes[i % len(pipes)], cfg)
     ms = statistics.mean(time_steps(lib, pipes, cfg, steps, flush, stream))
     kernel = lib.last_kernel()
+    # back-to-back: 20 launches between two events (the launches overlap their
+    # ramp and tail; rotating sets or a flush-free run over > L2 inputs)
+    b2b = None
+    if len(pipes) > 1:
+        a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(int(4e6))
+        a.record(stream)
+        for i in range(20):
+            lib.execute_fused(pipes[i % len(pipes)], cfg)
+        e.record(stream)
+        torch.cuda.synchronize()
+        b2b = a.elapsed_time(e) / 20
     lib.execute_unfused(w.pipeline, cfg)
     ums = statistics.mean(time_steps(lib, pipes, cfg, 3, flush, stream, lib.execute_unfused))
     peak, _ = measured_peak()
@@ -269,6 +281,24 @@ def sub_result(lib, cfg, stream, flush, workload, n_ops=64, crops=8192, steps=10
            "unfused": {"ms_per_step": ums, "speedup_fused_vs_unfused": ums / ms,
                        "kernels_per_step": w.pipeline.n_compute + 1},
            "cpu_baseline": cpu, "speedup_vs_cpu": mpix / cpu["value"]}
+    if b2b is not None:
+        out["back_to_back_ms_per_step"] = b2b
+        out["back_to_back_frac_of_measured_peak"] = w.alg_bytes / (b2b / 1e3) / 1e9 / peak
+    if workload == "c1":
+        # the same traffic through one PyTorch kernel (33.2 MB f32 read, 8.3 MB u8 write):
+        # what a single 41 MB launch costs on this GPU, launch and ramp included
+        src = torch.rand(2160, 3840, device="cuda")
+        srcs = [src, torch.rand_like(src), torch.rand_like(src), torch.rand_like(src)]
+        for s in srcs:
+            s.to(torch.uint8)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        torch.cuda._sleep(int(2e6))
+        for i, (a, e) in enumerate(evs):
+            a.record(stream)
+            srcs[i % 4].to(torch.uint8)
+            e.record(stream)
+        torch.cuda.synchronize()
+        out["torch_same_traffic_ms"] = statistics.mean(a.elapsed_time(e) for a, e in evs)
     if workload == "c3":
         # FP32 roofline above N ~ 45: N * P ops at the FMA pipe's packed rate
         out["fp32_ops"] = n_ops * w.points
