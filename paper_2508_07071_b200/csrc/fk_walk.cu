@@ -249,9 +249,9 @@ struct RowReg {  // a WalkRow in registers, fy as a packed pair
   uint32_t r1;
   uint64_t fy2;
 };
-__device__ __forceinline__ RowReg ld_row(const WalkRow* p) {
-  const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
-  return RowReg{v.x, (uint64_t(v.w) << 32) | v.z};
+__device__ __forceinline__ RowReg ld_row(const uint2* rows, uint32_t i) {  // from the unit's shared copy
+  const uint2 v = rows[i];
+  return RowReg{v.x, p2::pack(__uint_as_float(v.y), __uint_as_float(v.y))};
 }
 // base + a * b in one IMAD.WIDE (the compiler would share a * b across the three planes)
 __device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t base) {
@@ -282,8 +282,9 @@ __device__ __forceinline__ void h_row(uint32_t base, const uint32_t (&w)[2], con
 
 // Per-warp shared memory: the ring (kWalkSlots slots x 2 halves x kWalkGroup
 // rows), the slots' mbarriers, lane 0's staging arguments, the fix masks (one
-// lane mask per output row of the unit), slack for the last row's 12-byte
-// window; 128-byte aligned (TMA destinations).
+// lane mask per output row of the unit), the unit's row entries (r1, fy: the
+// walk reads them on its critical path, an L2 round trip from the table), slack
+// for the last row's 12-byte window; 128-byte aligned (TMA destinations).
 struct StageArgs {
   uint64_t map0, map1;  // tensor maps of the two halves' planes
   uint32_t bx0, bx1;    // box x of each half
@@ -293,7 +294,8 @@ struct StageArgs {
 __host__ __device__ constexpr uint32_t walk_half_bytes(uint32_t rb) { return (kWalkGroup * rb + 127) / 128 * 128; }
 __host__ __device__ constexpr uint32_t walk_ring_bytes(uint32_t rb) { return kWalkSlots * 2 * walk_half_bytes(rb); }
 __host__ __device__ constexpr uint32_t walk_warp_bytes(uint32_t rb, uint32_t max_rows) {
-  return (walk_ring_bytes(rb) + 8 * kWalkSlots + uint32_t(sizeof(StageArgs)) + 4 * max_rows + 16 + 127) / 128 * 128;
+  return (walk_ring_bytes(rb) + 8 * kWalkSlots + uint32_t(sizeof(StageArgs)) + 4 * (max_rows + 1) + 8 * (max_rows + 2) +
+          16 + 127) / 128 * 128;
 }
 
 // ------------------------------------------------------------------ kernel --
@@ -383,9 +385,15 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   for (uint32_t g = 0; g < kWalkSlots && g < ngroups; ++g) stage(g);
   const uint32_t y_hi = U.y_hi, y_lo = U.y_lo;
   uint32_t y = y_lo;
-  const WalkRow* rp = P.rows + U.rowtab + y;  // row table, walked with y
-  RowReg R = ld_row(rp);
+  // the unit's row entries y_lo .. y_hi (one past: the table's next row or sentinel) in shared memory
+  uint2* rows = reinterpret_cast<uint2*>(fixm + ((P.max_rows + 1) & ~1u));  // 8-byte aligned
+  for (uint32_t i = lane; i <= y_hi - y_lo; i += 32) {
+    const WalkRow& e = P.rows[U.rowtab + y_lo + i];
+    rows[i] = make_uint2(__ldg(&e.r1), __float_as_uint(__ldg(&e.fy)));
+  }
   for (uint32_t i = lane; i < y_hi - y_lo; i += 32) fixm[i] = 0;
+  __syncwarp();
+  RowReg R = ld_row(rows, 0);
   __syncwarp();
 
   // finish output row y from the H rows of its two source rows (a clamped row
@@ -404,7 +412,7 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
       const uint64_t e = p2::sub(v, k);
       flag = flag || fabsf(p2::lo(e)) > t0 || fabsf(p2::hi(e)) > t1;
       const uint64_t o = chain2<SIG>(k, ks, m);
-      if (active) st_cs2(mad_wide(y, dpitch, dst[m]), o);
+      if (active) __stcs(reinterpret_cast<float2*>(mad_wide(y, dpitch, dst[m])), make_float2(p2::lo(o), p2::hi(o)));
     }
     if (flag && active) atomicOr(fixm + (y - y_lo), 1u << lane);  // rare: fixed after the walk
   };
@@ -424,7 +432,7 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
     const uint32_t r = r_first + k;
     while (y < y_hi && (R.r1 & kWalkRowMask) == r) {
       const RowReg Rc = R;
-      R = ld_row(++rp);  // the next row's entry, in flight during the finish (sentinel past out_h)
+      R = ld_row(rows, y + 1 - y_lo);  // the next row's entry (the copy ends one past y_hi)
       finish(Hp, Hn, Rc);
       ++y;
     }
