@@ -339,13 +339,13 @@ WalkCol walk_col(uint32_t x, uint32_t rect_w, uint32_t out_w) {
     c.wts = (16384u - j) | (j << 16);
     c.s = 1.0f / 16384.0f;
     c.c = -512.0f;
-    c.thr = 0.5f;
+    c.thr = -__builtin_bit_cast(float, kWalkOff2Bits);
   } else {
     const uint32_t K = uint32_t(8388607 / (255 * den));
     c.wts = uint32_t(K * (den - nx)) | (uint32_t(K * nx) << 16);
     c.s = float(1.0 / double(K * den));
     c.c = float(-8388608.0 / double(K * den));
-    c.thr = kWalkThr;
+    c.thr = -__builtin_bit_cast(float, kWalkThr2Bits);
   }
   return c;
 }
@@ -406,7 +406,7 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   }
   for (const DWrite& w : writes)
     ok = ok && (w.flags & WF_ACTIVE) && w.pitch[0] == w.pitch[1] && w.pitch[0] == w.pitch[2] &&
-         (w.pitch[0] & 7) == 0 && w.pitch[0] < (1ull << 32) && ((w.dst[0] | w.dst[1] | w.dst[2]) & 7) == 0;
+         (w.pitch[0] & 7) == 0 && w.pitch[0] * H < (1ull << 32) && ((w.dst[0] | w.dst[1] | w.dst[2]) & 7) == 0;
   if (!ok) return false;
   // chain: the AFFINE signature with the verified division forms
   uint32_t fn[4] = {0, 0, 0, 0}, fast = 0, two = 0;
@@ -501,23 +501,47 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
       }
     }
   }
-  // TMA tensor maps: per plane, its crop's rows [y0, y0 + rect_h) as elements
-  // of 2, 4 or 8 bytes (the smallest whose 256-element box holds a staged row)
-  // over [0, ceil(3 (x0 + rect_w) / elem)): the last element of a row may
-  // extend past the crop, so that byte range must be readable in its last row
+  // TMA tensor maps: one per source frame (buffer, pitch), its rows [0, rows)
+  // as elements of 2, 4 or 8 bytes (the smallest whose 256-element box holds a
+  // staged row) over [0, width): rows = the lowest crop bottom, width = the
+  // widest crop's right edge rounded up to an element. The tensor's last
+  // element of a row may extend past a crop, so that byte range must be
+  // readable: every row but the frame's last has a row below it (pitch bytes),
+  // the last row its crop's tail_bytes. One map per frame keeps the TMA
+  // descriptor cache warm (one per crop missed on every copy).
   const uint32_t elem = row_bytes <= 512 ? 2 : row_bytes <= 1024 ? 4 : 8;
   if (!ok || units.empty() || row_bytes > 256 * elem) return false;
   if (walk_smem_bytes(row_bytes, band_rows) > 200 * 1024) return false;
-  std::vector<CUtensorMap> maps(B);
-  for (uint32_t z = 0; z < B && ok; ++z) {
+  struct Frame { uint64_t rows = 0, width = 0, tail = ~0ull; };
+  std::map<std::pair<uint64_t, uint64_t>, uint32_t> frame_at;
+  std::vector<Frame> frames;
+  std::vector<uint32_t> frame_of(B);
+  for (uint32_t z = 0; z < B; ++z) {
     const DSample& s = dp.reads[z];
-    const uint64_t end = 3ull * (s.x0 + s.rect_w), width = (end + elem - 1) / elem;
-    ok = width * elem <= s.tail_bytes &&
-         walk_encode_map(&maps[z], s.src + uint64_t(s.y0) * s.pitch, width, s.rect_h, s.pitch, elem,
-                         row_bytes / elem, kWalkGroup);
+    auto f = frame_at.emplace(std::make_pair(s.src, s.pitch), uint32_t(frames.size())).first;
+    if (f->second == frames.size()) frames.push_back(Frame{});
+    frame_of[z] = f->second;
+    Frame& fr = frames[f->second];
+    const uint64_t bottom = uint64_t(s.y0) + s.rect_h, end = 3ull * (s.x0 + s.rect_w);
+    if (bottom > fr.rows) fr.rows = bottom, fr.tail = s.tail_bytes;
+    else if (bottom == fr.rows) fr.tail = std::min<uint64_t>(fr.tail, s.tail_bytes);
+    fr.width = std::max(fr.width, (end + elem - 1) / elem);
+    ok = ok && s.pitch <= 0xffffffffull;
+  }
+  std::vector<CUtensorMap> maps(frames.size());
+  for (size_t f = 0; f < frames.size() && ok; ++f) {
+    const Frame& fr = frames[f];
+    const uint64_t src = dp.reads[std::find(frame_of.begin(), frame_of.end(), uint32_t(f)) - frame_of.begin()].src;
+    const uint64_t pitch = dp.reads[std::find(frame_of.begin(), frame_of.end(), uint32_t(f)) - frame_of.begin()].pitch;
+    ok = fr.width * elem <= std::min<uint64_t>(fr.tail, pitch) && f < 65536 &&
+         walk_encode_map(&maps[f], src, fr.width, fr.rows, pitch, elem, row_bytes / elem, kWalkGroup);
   }
   for (WalkUnit& u : units)
-    for (int h = 0; h < 2; ++h) u.bx[h] = uint16_t(u.bx[h] * 2 / elem);  // bx was in 2-byte elements
+    for (int h = 0; h < 2; ++h) {
+      u.bx[h] = uint16_t(u.bx[h] * 2 / elem);  // bx was in 2-byte elements
+      u.map[h] = uint16_t(frame_of[u.z[h]]);
+      u.y0[h] = dp.reads[u.z[h]].y0;
+    }
   if (!ok) return false;
   // units of one source frame back to back (the frame stays L2-resident while
   // its crops run), longest first within a frame (walk cost ~ visits + rows)
@@ -578,6 +602,8 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   P.elem = elem;
   P.negz = kNegZero2;
   P.max_rows = band_rows;
+  P.sink = reinterpret_cast<uint64_t>(upload(std::vector<uint64_t>(4, 0)));
+  dp.extra.push_back(reinterpret_cast<void*>(P.sink));
   wsig_out = wsig;
   perz_out = perz;
   return true;

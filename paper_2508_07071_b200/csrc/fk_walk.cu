@@ -9,11 +9,11 @@
 // lanes — and a band of output rows. Bilinear is separable; the warp walks the
 // source rows the band needs, top to bottom, each visited ONCE:
 //
-//   stage   lane 0 copies 4 source rows of each half's byte span at a time
+//   stage   lane 0 copies kWalkGroup source rows of each half's byte span at a time
 //           into a per-warp shared-memory ring, one 2D TMA tensor copy per
 //           half (cp.async.bulk.tensor, the crop's rows as a tensor map; rows
 //           and bytes outside the crop read as zeros), completion on an
-//           mbarrier, 4-8 rows ahead (no LSU traffic, no registers);
+//           mbarrier, one or two boxes ahead (no LSU traffic, no registers);
 //   H       each lane lerps row r horizontally at its two columns as exact
 //           integers: three 32-bit shared loads, a funnel shift to the
 //           column's byte offset, two byte_perm and three dp2a per column
@@ -58,9 +58,6 @@ __host__ __device__ constexpr bool div2(uint32_t sig, int k) { return (sig >> (k
 
 // The chain's constants for input lane m, op k, as pairs: c, and for a division
 // either (r_hi, r_lo) [two-op form] or (RN(1/c), -c) [three-op form].
-#ifndef FK_WALK_PEEL
-#define FK_WALK_PEEL 1
-#endif
 #ifndef FK_WALK_KREG
 #define FK_WALK_KREG 0  // 1: chain constants held in registers (measured slower: 1.46 vs 1.39 ms on C5)
 #endif
@@ -227,40 +224,23 @@ __device__ __forceinline__ void tma_rows(uint32_t dst, uint64_t map, uint32_t x,
 }
 // One elected lane: expect `tx` bytes on mbar, copy half 0's box to dst and, if
 // off1 != 0, half 1's box to dst + off1 (all operands warp-uniform).
-__device__ __forceinline__ void tma_group(uint32_t dst, uint64_t m0, uint32_t x0, uint64_t m1, uint32_t x1, uint32_t y,
-                                          uint32_t mbar, uint32_t tx, uint32_t off1) {
+__device__ __forceinline__ void tma_group(uint32_t dst, uint64_t m0, uint32_t x0, uint32_t y0, uint64_t m1, uint32_t x1,
+                                          uint32_t y1, uint32_t mbar, uint32_t tx, uint32_t off1) {
   asm volatile(
       "{\n\t.reg .pred p, q;\n\t"
       "elect.sync _|p, 0xffffffff;\n\t"
-      "setp.ne.and.u32 q, %8, 0, p;\n\t"
-      "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%6], %7;\n\t"
-      "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %5}], [%6];\n\t"
-      "@q cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%9], [%3, {%4, %5}], [%6];\n\t"
+      "setp.ne.and.u32 q, %9, 0, p;\n\t"
+      "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%7], %8;\n\t"
+      "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%7];\n\t"
+      "@q cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%10], [%4, {%5, %6}], [%7];\n\t"
       "}" ::"r"(dst),
-      "l"(m0), "r"(x0), "l"(m1), "r"(x1), "r"(y), "r"(mbar), "r"(tx), "r"(off1), "r"(dst + off1)
+      "l"(m0), "r"(x0), "r"(y0), "l"(m1), "r"(x1), "r"(y1), "r"(mbar), "r"(tx), "r"(off1), "r"(dst + off1)
       : "memory");
 }
 __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   uint32_t v;
   asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(a));
   return v;
-}
-struct RowReg {  // a WalkRow in registers, fy as a packed pair
-  uint32_t r1;
-  uint64_t fy2;
-};
-__device__ __forceinline__ RowReg ld_row(const uint2* rows, uint32_t i) {  // from the unit's shared copy
-  const uint2 v = rows[i];
-  return RowReg{v.x, p2::pack(__uint_as_float(v.y), __uint_as_float(v.y))};
-}
-// base + a * b in one IMAD.WIDE (the compiler would share a * b across the three planes)
-__device__ __forceinline__ uint64_t mad_wide(uint32_t a, uint32_t b, uint64_t base) {
-  uint64_t d;
-  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(base));
-  return d;
-}
-__device__ __forceinline__ void st_cs2(uint64_t addr, uint64_t v) {
-  asm volatile("st.global.cs.b64 [%0], %1;" ::"l"(addr), "l"(v) : "memory");
 }
 
 // H of one visited source row at the lane's two columns: three exact integers
@@ -286,8 +266,9 @@ __device__ __forceinline__ void h_row(uint32_t base, const uint32_t (&w)[2], con
 // walk reads them on its critical path, an L2 round trip from the table), slack
 // for the last row's 12-byte window; 128-byte aligned (TMA destinations).
 struct StageArgs {
-  uint64_t map0, map1;  // tensor maps of the two halves' planes
+  uint64_t map0, map1;  // tensor maps of the two halves' frames
   uint32_t bx0, bx1;    // box x of each half
+  uint32_t y0, y1;      // TMA y of each half's source row r_first
   uint32_t two;         // half 1 present
   uint32_t pad;
 };
@@ -322,7 +303,9 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   const uint32_t xh = h ? U.x[1] : U.x[0];
   const uint32_t x = xh + 2u * (h ? lane - n0 : lane);
   const WalkAux A = P.aux[z];
-  // column constants (inactive lanes duplicate a valid column; they never store)
+  // column constants. An idle lane lerps a valid column with s = c = 0 (v = 0:
+  // never flagged) and stores to the plan's sink with a zero row step, so the
+  // finish carries no store predicate.
   uint32_t w[2], sh[2], wts[2];
   float s[2], c[2], tc[2];
 #pragma unroll
@@ -332,32 +315,40 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
     w[k] = (rel & ~3u) + (h ? HB : 0u);
     sh[k] = (rel & 3u) * 8u;
     wts[k] = C.wts;
-    s[k] = C.s;
-    c[k] = C.c;
+    s[k] = active ? C.s : 0.0f;
+    c[k] = active ? C.c : 0.0f;
     tc[k] = C.thr;
   }
   const uint64_t s2 = p2::pack(s[0], s[1]), c2 = p2::pack(c[0], c[1]);
   const uint64_t kR = p2::pack(kRound, kRound);
-  uint64_t dst[3];
+  const uint64_t nT_col = p2::pack(tc[0], tc[1]);
+  const float nthr = -__uint_as_float(kWalkThr2Bits);
+  const uint64_t nT_thr = p2::pack(nthr, nthr);
+  const uint32_t y_hi = U.y_hi, y_lo = U.y_lo;
+  const uint32_t dstep = active ? A.dpitch : 0u;
+  uint64_t dst[3];  // the lane's column pair in row y_lo of each plane; row y at dst + yoff
 #pragma unroll
-  for (int m = 0; m < 3; ++m) dst[m] = P.dst_base + A.dst[m] + 4ull * x;
-  const uint32_t dpitch = A.dpitch;
+  for (int m = 0; m < 3; ++m) dst[m] = active ? P.dst_base + A.dst[m] + 4ull * x + uint64_t(y_lo) * A.dpitch : P.sink;
+  uint32_t yoff = 0;  // (y - y_lo) * dstep: a plane is < 4 GiB
   using KS = typename std::conditional<PERZ, KReg<SIG>, KInl<SIG>>::type;
   const KS ks = [&]() {
     if constexpr (PERZ) return KReg<SIG>(P.kz + 12ull * A.kz, P.negz);
     else return KInl<SIG>(P, P.negz);
   }();
 
-  // lane 0 stages group g (source rows r_first + 4 g ...) into ring slot g % 2,
-  // both halves on that slot's mbarrier; its arguments wait in shared memory
+  // lane 0 stages group g (source rows r_first + kWalkGroup g ...) into ring
+  // slot g % 2, both halves on that slot's mbarrier; its arguments wait in
+  // shared memory
   const uint32_t r_first = U.r_first;
   const uint32_t nvis = uint32_t(U.r_last) - r_first + 1u, ngroups = (nvis + kWalkGroup - 1) / kWalkGroup;
   if (lane == 0) {
     StageArgs t;
-    t.map0 = reinterpret_cast<uint64_t>(P.maps + U.z[0]);
-    t.map1 = reinterpret_cast<uint64_t>(P.maps + U.z[1]);
+    t.map0 = reinterpret_cast<uint64_t>(P.maps + U.map[0]);
+    t.map1 = reinterpret_cast<uint64_t>(P.maps + U.map[1]);
     t.bx0 = U.bx[0];
     t.bx1 = U.bx[1];
+    t.y0 = U.y0[0] + r_first;
+    t.y1 = U.y0[1] + r_first;
     t.two = U.n[1] != 0;
     *sa = t;
   }
@@ -370,11 +361,12 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
     const uint32_t bx0 = __shfl_sync(0xffffffffu, t.bx0, 0), bx1 = __shfl_sync(0xffffffffu, t.bx1, 0);
     const uint32_t two = __shfl_sync(0xffffffffu, t.two, 0);
     const uint32_t slot = g % kWalkSlots;
-    const uint32_t r = __shfl_sync(0xffffffffu, r_first, 0) + g * kWalkGroup;
+    const uint32_t y0 = __shfl_sync(0xffffffffu, t.y0, 0) + g * kWalkGroup;
+    const uint32_t y1 = __shfl_sync(0xffffffffu, t.y1, 0) + g * kWalkGroup;
     const uint32_t mb = __shfl_sync(0xffffffffu, bar, 0) + 8 * slot;
     const uint32_t dst = __shfl_sync(0xffffffffu, ring, 0) + slot * GB;
     const uint32_t box = kWalkGroup * RB;  // bytes one box delivers (zero-filled outside the crop)
-    tma_group(dst, m0, bx0, m1, bx1, r, mb, two ? 2 * box : box, two ? HB : 0u);
+    tma_group(dst, m0, bx0, y0, m1, bx1, y1, mb, two ? 2 * box : box, two ? HB : 0u);
   };
   if (lane == 0) {
 #pragma unroll
@@ -383,26 +375,24 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   }
   __syncwarp();
   for (uint32_t g = 0; g < kWalkSlots && g < ngroups; ++g) stage(g);
-  const uint32_t y_hi = U.y_hi, y_lo = U.y_lo;
-  uint32_t y = y_lo;
-  // the unit's row entries y_lo .. y_hi (one past: the table's next row or sentinel) in shared memory
+  // the unit's row entries (r1, fy) y_lo .. y_hi - 1 and a sentinel in shared memory
   uint2* rows = reinterpret_cast<uint2*>(fixm + ((P.max_rows + 1) & ~1u));  // 8-byte aligned
-  for (uint32_t i = lane; i <= y_hi - y_lo; i += 32) {
+  const uint32_t nrows = y_hi - y_lo;
+  for (uint32_t i = lane; i <= nrows; i += 32) {
     const WalkRow& e = P.rows[U.rowtab + y_lo + i];
-    rows[i] = make_uint2(__ldg(&e.r1), __float_as_uint(__ldg(&e.fy)));
+    rows[i] = i < nrows ? make_uint2(__ldg(&e.r1), __float_as_uint(__ldg(&e.fy))) : make_uint2(kWalkRowMask, 0u);
   }
-  for (uint32_t i = lane; i < y_hi - y_lo; i += 32) fixm[i] = 0;
+  for (uint32_t i = lane; i < nrows; i += 32) fixm[i] = 0;
   __syncwarp();
-  RowReg R = ld_row(rows, 0);
-  __syncwarp();
+  uint32_t ri = 0;  // the next output row's entry (y - y_lo)
+  uint2 R = rows[0];
 
-  // finish output row y from the H rows of its two source rows (a clamped row
-  // has fy = 1: Ha + (Hb - Ha) * 1 == Hb exactly)
-  auto finish = [&](const float (&Ha)[2][3], const float (&Hb)[2][3], const RowReg& Rw) {
-    const uint64_t fy2 = Rw.fy2;
-    const bool exact_row = Rw.r1 & kWalkExactRow;
-    const float t0 = exact_row ? tc[0] : kWalkThr, t1 = exact_row ? tc[1] : kWalkThr;
-    bool flag = false;
+  // finish the output row of entry (r1, fy) from the H rows of its two source
+  // rows (a clamped row has fy = 1: Ha + (Hb - Ha) * 1 == Hb exactly)
+  auto finish = [&](const float (&Ha)[2][3], const float (&Hb)[2][3], uint32_t r1, float fy) {
+    const uint64_t fy2 = p2::pack(fy, fy);
+    const uint64_t nT = (r1 & kWalkExactRow) ? nT_col : nT_thr;
+    uint32_t acc = 0xffffffffu;  // AND of the filter values' sign bits: clear = flagged
 #pragma unroll
     for (int m = 0; m < 3; ++m) {
       const uint64_t a2 = p2::pack(Ha[0][m], Ha[1][m]), b2 = p2::pack(Hb[0][m], Hb[1][m]);
@@ -410,49 +400,36 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
       const uint64_t v = p2::fma(p, s2, c2);                  // pixel units
       const uint64_t k = p2::sub(p2::add(v, kR), kR);         // rint(v): the u8 result, as f32
       const uint64_t e = p2::sub(v, k);
-      flag = flag || fabsf(p2::lo(e)) > t0 || fabsf(p2::hi(e)) > t1;
+      const uint64_t q = p2::fma(e, e, nT);                   // e^2 - T
+      acc &= uint32_t(q) & uint32_t(q >> 32);
       const uint64_t o = chain2<SIG>(k, ks, m);
-      if (active) __stcs(reinterpret_cast<float2*>(mad_wide(y, dpitch, dst[m])), make_float2(p2::lo(o), p2::hi(o)));
+      __stcs(reinterpret_cast<float2*>(dst[m] + yoff), make_float2(p2::lo(o), p2::hi(o)));
     }
-    if (flag && active) atomicOr(fixm + (y - y_lo), 1u << lane);  // rare: fixed after the walk
+    yoff += dstep;
+    if (int32_t(acc) >= 0) atomicOr(fixm + ri, 1u << lane);  // rare (a flagged value): recomputed after the walk
   };
 
   float HA[2][3], HB2[2][3];
-  // visit k (row staged at `row`): H into Hn, then every output row it completes
-  auto visit = [&](uint32_t k, uint32_t row, float (&Hn)[2][3], float (&Hp)[2][3]) {
+  // visit source row r (staged at `row`): H into Hn, then every output row it completes
+  auto visit = [&](uint32_t r, uint32_t row, float (&Hn)[2][3], float (&Hp)[2][3]) {
     h_row(row, w, sh, wts, Hn);
-#if !FK_WALK_PEEL
-    if (k == 0) {
-#pragma unroll
-      for (int i = 0; i < 2; ++i)
-#pragma unroll
-        for (int m = 0; m < 3; ++m) Hp[i][m] = Hn[i][m];
-    }
-#endif
-    const uint32_t r = r_first + k;
-    while (y < y_hi && (R.r1 & kWalkRowMask) == r) {
-      const RowReg Rc = R;
-      R = ld_row(rows, y + 1 - y_lo);  // the next row's entry (the copy ends one past y_hi)
-      finish(Hp, Hn, Rc);
-      ++y;
+    while ((R.x & kWalkRowMask) == r) {
+      finish(Hp, Hn, R.x, __uint_as_float(R.y));
+      R = rows[++ri];
     }
   };
   // visit 0's "previous" row is row 0 itself (only a clamped row completes there)
-#if FK_WALK_PEEL
   mbar_wait(bar, 0);
   h_row(ring, w, sh, wts, HB2);
-#endif
+  // whole groups: visits past r_last read staged rows but complete nothing (the sentinel)
   for (uint32_t g = 0; g < ngroups; ++g) {
     const uint32_t slot = g % kWalkSlots;
     mbar_wait(bar + 8 * slot, (g / kWalkSlots) & 1u);
-#pragma unroll 1
-    for (uint32_t q = 0; q < kWalkGroup; q += 4) {
-      const uint32_t k = g * kWalkGroup + q, row = ring + slot * GB + q * RB;
-      if (k >= nvis) break;
-      visit(k, row, HA, HB2);
-      if (k + 1 < nvis && q + 1 < kWalkGroup) visit(k + 1, row + RB, HB2, HA);
-      if (k + 2 < nvis && q + 2 < kWalkGroup) visit(k + 2, row + 2 * RB, HA, HB2);
-      if (k + 3 < nvis && q + 3 < kWalkGroup) visit(k + 3, row + 3 * RB, HB2, HA);
+    const uint32_t row = ring + slot * GB, r = r_first + g * kWalkGroup;
+#pragma unroll
+    for (uint32_t q = 0; q < kWalkGroup; q += 2) {
+      visit(r + q, row + q * RB, HA, HB2);
+      visit(r + q + 1, row + (q + 1) * RB, HB2, HA);
     }
     __syncwarp();  // every lane is done with the slot
     if (g + kWalkSlots < ngroups) stage(g + kWalkSlots);

@@ -27,6 +27,11 @@ constexpr uint32_t kWalkHalfLanes = 16;          // lanes per half-warp strip (2
 constexpr uint32_t kWalkMaxRows = FK_WALK_MAXROWS;  // output rows per unit (bounds the fix masks)
 constexpr uint32_t kWalkBias = 0x4B000000u;      // bit pattern of 2^23: H values are biased floats
 constexpr float kWalkThr = 0.5f - 1.0f / 8192.0f;  // exact-result filter: 0.5 - E, E = 2^-13
+// The filter squared: a value is flagged when fma(e, e, -T) >= 0 (e = v - rint(v)),
+// i.e. |e| >= sqrt(T). T = kWalkThr^2 = 1/4 - 2^-13 + 2^-26 is exact in f32
+// (0x3e7fe001); an exact column of an exact row uses T = RN_up(1/4) (never flagged).
+constexpr uint32_t kWalkThr2Bits = 0x3e7fe001u;
+constexpr uint32_t kWalkOff2Bits = 0x3e800001u;
 
 // One output column x of a (rect_w, out_w) table. Horizontal lerp of source row
 // r as ONE exact integer per lane: H = wa * a + wb * b (dp2a), with
@@ -42,7 +47,7 @@ struct WalkCol {
   uint32_t tap;   // 3 * ix0 (clamped), bytes from the crop's left edge
   uint32_t wts;   // dp2a weights wa | wb << 16 (wb = 0 when both taps clamp to one column)
   float s, c;     // pixel scale of H, see above
-  float thr;      // 0.5 (exact column) or 0.5 - E: the exact-result filter threshold
+  float thr;      // -T of the exact-result filter on an exact row: -kWalkOff2 (exact column) or -kWalkThr2
   uint32_t pad[3];
 };
 // One output row y of a (rect_h, out_h) table: the row completes when the walk
@@ -74,9 +79,11 @@ struct WalkAux {
 // same rect_h) share the row table and the visit walk; each has its own TMA box.
 struct WalkUnit {
   uint32_t z[2];
-  uint16_t bx[2];       // TMA box x (in elements): the staged span starts at byte elem * bx of the crop row
+  uint32_t y0[2];       // TMA y of each half's source row 0 (the crop's top row in its frame)
+  uint16_t bx[2];       // TMA box x (in elements): the staged span starts at byte elem * bx of the frame row
   uint16_t x[2];        // first output column of each half
   uint16_t n[2];        // lanes of each half (n[1] = 0: one plane)
+  uint16_t map[2];      // tensor map (WalkPlan::maps) of each half's source frame
   uint16_t y_lo, y_hi;  // output rows
   uint16_t r_first, r_last;  // source rows visited (relative to y0)
   uint32_t rowtab;      // WalkRow index of output row 0
@@ -87,7 +94,7 @@ struct WalkPlan {
   const WalkAux* aux;
   const WalkCol* cols;
   const WalkRow* rows;
-  const CUtensorMap* maps;  // per plane: its crop's rows as a 2D tensor of elem-byte elements (rect_h rows)
+  const CUtensorMap* maps;  // per source frame (buffer and pitch): its rows as a 2D tensor of elem-byte elements
   const DSample* reads;     // exact-fix path (reference arithmetic)
   const float4* kz;         // per-plane constants [kz][op][lane] = (c, r_hi, r_lo, 0), input-lane order; or null
   uint32_t n_units;
@@ -96,6 +103,7 @@ struct WalkPlan {
   uint32_t elem;            // tensor-map element bytes (2, 4 or 8)
   uint64_t negz;            // kNegZero2 (fk_pack2.cuh): a product's runtime -0 addend
   uint64_t dst_base;        // added to every WalkAux::dst (0: absolute; the unfused pass 0: its intermediate)
+  uint64_t sink;            // 8-byte scratch the idle lanes of a unit store to (no store predicate)
   // inline chain constants (shared by every plane), input-lane order, as pairs
   float2 kc[4][3], kh[4][3], kl[4][3];
 };
