@@ -261,10 +261,11 @@ __device__ __forceinline__ void h_row(uint32_t base, const uint32_t (&w)[2], con
 }
 
 // Per-warp shared memory: the ring (kWalkSlots slots x 2 halves x kWalkGroup
-// rows), the slots' mbarriers, lane 0's staging arguments, the fix masks (one
-// lane mask per output row of the unit), the unit's row entries (r1, fy: the
-// walk reads them on its critical path, an L2 round trip from the table), slack
-// for the last row's 12-byte window; 128-byte aligned (TMA destinations).
+// rows), the slots' mbarriers and lane 0's staging arguments (64 bytes), the
+// unit's row entries (RowEnt: the walk reads them on its critical path, an L2
+// round trip from the table) and a sentinel, the fix masks (one lane mask per
+// output row of the unit), slack for the last row's 12-byte window; 128-byte
+// aligned (TMA destinations).
 struct StageArgs {
   uint64_t map0, map1;  // tensor maps of the two halves' frames
   uint32_t bx0, bx1;    // box x of each half
@@ -274,9 +275,16 @@ struct StageArgs {
 };
 __host__ __device__ constexpr uint32_t walk_half_bytes(uint32_t rb) { return (kWalkGroup * rb + 127) / 128 * 128; }
 __host__ __device__ constexpr uint32_t walk_ring_bytes(uint32_t rb) { return kWalkSlots * 2 * walk_half_bytes(rb); }
+struct RowEnt {        // a WalkRow as the walk reads it: one 16-byte shared load
+  uint32_t r1;          // source row that completes the output row (kWalkRowMask: sentinel)
+  float fy;
+  uint32_t exact;       // kWalkExactRow set: the exact-column filter applies
+  uint32_t pad;
+};
+constexpr uint32_t kWalkMeta = 64;  // mbarriers + StageArgs
+static_assert(8 * kWalkSlots + sizeof(StageArgs) <= kWalkMeta, "walk meta");
 __host__ __device__ constexpr uint32_t walk_warp_bytes(uint32_t rb, uint32_t max_rows) {
-  return (walk_ring_bytes(rb) + 8 * kWalkSlots + uint32_t(sizeof(StageArgs)) + 4 * (max_rows + 1) + 8 * (max_rows + 2) +
-          16 + 127) / 128 * 128;
+  return (walk_ring_bytes(rb) + kWalkMeta + 16 * (max_rows + 1) + 4 * max_rows + 16 + 127) / 128 * 128;
 }
 
 // ------------------------------------------------------------------ kernel --
@@ -292,7 +300,8 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   const uint32_t ring = uint32_t(__cvta_generic_to_shared(wbase));
   const uint32_t bar = ring + kWalkSlots * GB;
   StageArgs* sa = reinterpret_cast<StageArgs*>(wbase + kWalkSlots * GB + 8 * kWalkSlots);
-  uint32_t* fixm = reinterpret_cast<uint32_t*>(sa + 1);
+  RowEnt* rows = reinterpret_cast<RowEnt*>(wbase + kWalkSlots * GB + kWalkMeta);
+  uint32_t* fixm = reinterpret_cast<uint32_t*>(rows + P.max_rows + 1);
 
   // lane role: half h, plane z, output columns x, x + 1 (fields picked with
   // selects: a dynamic index into U would put it in local memory)
@@ -375,23 +384,23 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   }
   __syncwarp();
   for (uint32_t g = 0; g < kWalkSlots && g < ngroups; ++g) stage(g);
-  // the unit's row entries (r1, fy) y_lo .. y_hi - 1 and a sentinel in shared memory
-  uint2* rows = reinterpret_cast<uint2*>(fixm + ((P.max_rows + 1) & ~1u));  // 8-byte aligned
+  // the unit's row entries y_lo .. y_hi - 1 and a sentinel in shared memory
   const uint32_t nrows = y_hi - y_lo;
   for (uint32_t i = lane; i <= nrows; i += 32) {
     const WalkRow& e = P.rows[U.rowtab + y_lo + i];
-    rows[i] = i < nrows ? make_uint2(__ldg(&e.r1), __float_as_uint(__ldg(&e.fy))) : make_uint2(kWalkRowMask, 0u);
+    const uint32_t r1 = __ldg(&e.r1);
+    rows[i] = i < nrows ? RowEnt{r1 & kWalkRowMask, __ldg(&e.fy), r1 & kWalkExactRow, 0u}
+                        : RowEnt{kWalkRowMask, 0.0f, 0u, 0u};
   }
-  for (uint32_t i = lane; i < nrows; i += 32) fixm[i] = 0;
   __syncwarp();
   uint32_t ri = 0;  // the next output row's entry (y - y_lo)
-  uint2 R = rows[0];
+  RowEnt R = rows[0];
 
   // finish the output row of entry (r1, fy) from the H rows of its two source
   // rows (a clamped row has fy = 1: Ha + (Hb - Ha) * 1 == Hb exactly)
-  auto finish = [&](const float (&Ha)[2][3], const float (&Hb)[2][3], uint32_t r1, float fy) {
-    const uint64_t fy2 = p2::pack(fy, fy);
-    const uint64_t nT = (r1 & kWalkExactRow) ? nT_col : nT_thr;
+  auto finish = [&](const float (&Ha)[2][3], const float (&Hb)[2][3], const RowEnt& E) {
+    const uint64_t fy2 = p2::pack(E.fy, E.fy);
+    const uint64_t nT = E.exact ? nT_col : nT_thr;
     uint32_t acc = 0xffffffffu;  // AND of the filter values' sign bits: clear = flagged
 #pragma unroll
     for (int m = 0; m < 3; ++m) {
@@ -406,15 +415,17 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
       __stcs(reinterpret_cast<float2*>(dst[m] + yoff), make_float2(p2::lo(o), p2::hi(o)));
     }
     yoff += dstep;
-    if (int32_t(acc) >= 0) atomicOr(fixm + ri, 1u << lane);  // rare (a flagged value): recomputed after the walk
+    // the row's flagged lanes (rare; recomputed after the walk): every lane
+    // stores the same ballot, the row is finished exactly once
+    fixm[ri] = __ballot_sync(0xffffffffu, int32_t(acc) >= 0);
   };
 
   float HA[2][3], HB2[2][3];
   // visit source row r (staged at `row`): H into Hn, then every output row it completes
   auto visit = [&](uint32_t r, uint32_t row, float (&Hn)[2][3], float (&Hp)[2][3]) {
     h_row(row, w, sh, wts, Hn);
-    while ((R.x & kWalkRowMask) == r) {
-      finish(Hp, Hn, R.x, __uint_as_float(R.y));
+    while (R.r1 == r) {
+      finish(Hp, Hn, R);
       R = rows[++ri];
     }
   };
