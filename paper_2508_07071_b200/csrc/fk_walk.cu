@@ -223,16 +223,19 @@ __device__ __forceinline__ void tma_rows(uint32_t dst, uint64_t map, uint32_t x,
       : "memory");
 }
 // One elected lane: expect `tx` bytes on mbar, copy half 0's box to dst and, if
-// off1 != 0, half 1's box to dst + off1 (all operands warp-uniform).
+// off1 != 0, half 1's box to dst + off1 (all operands warp-uniform). The source
+// rows are read with an L2 evict_last policy: the frames stay resident while
+// the outputs stream past them (streaming stores are evict_first).
 __device__ __forceinline__ void tma_group(uint32_t dst, uint64_t m0, uint32_t x0, uint32_t y0, uint64_t m1, uint32_t x1,
                                           uint32_t y1, uint32_t mbar, uint32_t tx, uint32_t off1) {
   asm volatile(
-      "{\n\t.reg .pred p, q;\n\t"
+      "{\n\t.reg .pred p, q;\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
       "elect.sync _|p, 0xffffffff;\n\t"
       "setp.ne.and.u32 q, %9, 0, p;\n\t"
       "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%7], %8;\n\t"
-      "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%7];\n\t"
-      "@q cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%10], [%4, {%5, %6}], [%7];\n\t"
+      "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3}], [%7], pol;\n\t"
+      "@q cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%10], [%4, {%5, %6}], [%7], pol;\n\t"
       "}" ::"r"(dst),
       "l"(m0), "r"(x0), "r"(y0), "l"(m1), "r"(x1), "r"(y1), "r"(mbar), "r"(tx), "r"(off1), "r"(dst + off1)
       : "memory");
