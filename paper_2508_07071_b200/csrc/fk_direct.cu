@@ -35,11 +35,17 @@ constexpr int kChunks = kD / 4;
 #ifndef FK_DIRECT_TILES
 #define FK_DIRECT_TILES 1
 #endif
-#ifndef FK_DIRECT_MINB
-#define FK_DIRECT_MINB 6
-#endif
 constexpr int kTilesPerIter = FK_DIRECT_TILES;  // warp tiles loaded before any is computed
-constexpr int kDirectMinBlocks = FK_DIRECT_MINB;
+
+// Resident CTAs per SM: 5 (48 registers) for chains without a division, 4 (64
+// registers) for chains with one: at 6 / 5 the division chains spill 68-76
+// bytes (C1: 16.8 -> 15.0 us without the spills), while C3's long Mul/Add loop
+// wants the extra warps (74 us at 4 vs 42 us at 5).
+__host__ __device__ constexpr int direct_min_blocks(uint32_t sig) {
+  for (int k = 0; k < sig_n(sig); ++k)
+    if (sig_fn(sig, k) == AF_DIV) return 4;
+  return 5;
+}
 
 // registered chains; bit 12+k marks op k as a verified reciprocal division
 #define FK_DIRECT_SIGS(X)                                                                         \
@@ -255,7 +261,7 @@ __device__ __forceinline__ void finish_tile(const DPlan& P, const DWrite& w, Til
 // tail wave); two tiles in flight per warp: both tiles' loads are issued before
 // either is computed.
 template <uint32_t SIG, bool TO_U8>
-__global__ void __launch_bounds__(kBlock, kDirectMinBlocks) fk_direct(const __grid_constant__ DPlan P) {
+__global__ void __launch_bounds__(kBlock, direct_min_blocks(SIG)) fk_direct(const __grid_constant__ DPlan P) {
   // chain constants at fixed kernel-parameter offsets (constant-bank operands)
   const float c[4] = {P.aff_c[0][0], P.aff_c[1][0], P.aff_c[2][0], P.aff_c[3][0]};
   const float r[4] = {P.aff_r[0][0], P.aff_r[1][0], P.aff_r[2][0], P.aff_r[3][0]};
