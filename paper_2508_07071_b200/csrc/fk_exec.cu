@@ -602,7 +602,7 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   P.elem = elem;
   P.negz = kNegZero2;
   P.max_rows = band_rows;
-  P.sink = reinterpret_cast<uint64_t>(upload(std::vector<uint64_t>(4, 0)));
+  P.sink = reinterpret_cast<uint64_t>(upload(std::vector<uint64_t>(kWalkSinkLines * 32, 0)));
   dp.extra.push_back(reinterpret_cast<void*>(P.sink));
   wsig_out = wsig;
   perz_out = perz;

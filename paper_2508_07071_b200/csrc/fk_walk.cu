@@ -316,8 +316,10 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   const uint32_t x = xh + 2u * (h ? lane - n0 : lane);
   const WalkAux A = P.aux[z];
   // column constants. An idle lane lerps a valid column with s = c = 0 (v = 0:
-  // never flagged) and stores to the plan's sink with a zero row step, so the
-  // finish carries no store predicate.
+  // never flagged) and stores to its warp's line of the plan's sink with a zero
+  // row step, so the finish carries no store predicate. (One sink line shared by
+  // every warp was an L2 hot spot: B = 1024 crops, odd half counts per crop
+  // height, 212 -> 323 us.)
   uint32_t w[2], sh[2], wts[2];
   float s[2], c[2], tc[2];
 #pragma unroll
@@ -340,7 +342,9 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   const uint32_t dstep = active ? A.dpitch : 0u;
   uint64_t dst[3];  // the lane's column pair in row y_lo of each plane; row y at dst + yoff
 #pragma unroll
-  for (int m = 0; m < 3; ++m) dst[m] = active ? P.dst_base + A.dst[m] + 4ull * x + uint64_t(y_lo) * A.dpitch : P.sink;
+  for (int m = 0; m < 3; ++m)
+    dst[m] = active ? P.dst_base + A.dst[m] + 4ull * x + uint64_t(y_lo) * A.dpitch
+                    : P.sink + 256ull * (u % kWalkSinkLines) + 8 * lane;
   uint32_t yoff = 0;  // (y - y_lo) * dstep: a plane is < 4 GiB
   using KS = typename std::conditional<PERZ, KReg<SIG>, KInl<SIG>>::type;
   const KS ks = [&]() {

@@ -25,6 +25,7 @@ constexpr uint32_t kWalkHalfLanes = 16;          // lanes per half-warp strip (2
 #define FK_WALK_MAXROWS 112  // 112-row bands: twice the units of whole-plane walks, a shorter tail
 #endif
 constexpr uint32_t kWalkMaxRows = FK_WALK_MAXROWS;  // output rows per unit (bounds the fix masks)
+constexpr uint32_t kWalkSinkLines = 4096;         // one 256-byte line per warp (mod): no shared hot line
 constexpr uint32_t kWalkBias = 0x4B000000u;      // bit pattern of 2^23: H values are biased floats
 constexpr float kWalkThr = 0.5f - 1.0f / 8192.0f;  // exact-result filter: 0.5 - E, E = 2^-13
 // The filter squared: a value is flagged when fma(e, e, -T) >= 0 (e = v - rint(v)),
@@ -103,7 +104,8 @@ struct WalkPlan {
   uint32_t elem;            // tensor-map element bytes (2, 4 or 8)
   uint64_t negz;            // kNegZero2 (fk_pack2.cuh): a product's runtime -0 addend
   uint64_t dst_base;        // added to every WalkAux::dst (0: absolute; the unfused pass 0: its intermediate)
-  uint64_t sink;            // 8-byte scratch the idle lanes of a unit store to (no store predicate)
+  uint64_t sink;            // kWalkSinkLines x 256-byte scratch the idle lanes of a unit store to (no
+                            // store predicate): warp u's idle lanes write line u % kWalkSinkLines
   // inline chain constants (shared by every plane), input-lane order, as pairs
   float2 kc[4][3], kh[4][3], kl[4][3];
 };
