@@ -395,7 +395,8 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   const uint32_t W = p.space.width, H = p.space.height, B = p.space.batch;
   const uint32_t wid = p.write.id == FK_OP_BATCH_WRITE ? p.write.w_inner : p.write.id;
   if (!dp.affine_ok || dp.resample_lanes != 3 || wid != FK_OP_SPLIT_WRITE || B == 0 || W % 2 || W == 0 || H == 0 ||
-      W > 65534 || H > 65535 || lane_kind(uint32_t(p.write.in_kind)) != FK_F32)
+      W > 65534 || H > 65535 || 255ull * 2 * W > 8388607 /* K >= 1 in walk_col */ ||
+      lane_kind(uint32_t(p.write.in_kind)) != FK_F32)
     return false;
   bool ok = true;
   for (const DSample& s : dp.reads) {
@@ -512,14 +513,14 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   const uint32_t elem = row_bytes <= 512 ? 2 : row_bytes <= 1024 ? 4 : 8;
   if (!ok || units.empty() || row_bytes > 256 * elem) return false;
   if (walk_smem_bytes(row_bytes, band_rows) > 200 * 1024) return false;
-  struct Frame { uint64_t rows = 0, width = 0, tail = ~0ull; };
+  struct Frame { uint64_t src = 0, pitch = 0, rows = 0, width = 0, tail = ~0ull; };
   std::map<std::pair<uint64_t, uint64_t>, uint32_t> frame_at;
   std::vector<Frame> frames;
   std::vector<uint32_t> frame_of(B);
   for (uint32_t z = 0; z < B; ++z) {
     const DSample& s = dp.reads[z];
     auto f = frame_at.emplace(std::make_pair(s.src, s.pitch), uint32_t(frames.size())).first;
-    if (f->second == frames.size()) frames.push_back(Frame{});
+    if (f->second == frames.size()) frames.push_back(Frame{s.src, s.pitch});
     frame_of[z] = f->second;
     Frame& fr = frames[f->second];
     const uint64_t bottom = uint64_t(s.y0) + s.rect_h, end = 3ull * (s.x0 + s.rect_w);
@@ -531,10 +532,8 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   std::vector<CUtensorMap> maps(frames.size());
   for (size_t f = 0; f < frames.size() && ok; ++f) {
     const Frame& fr = frames[f];
-    const uint64_t src = dp.reads[std::find(frame_of.begin(), frame_of.end(), uint32_t(f)) - frame_of.begin()].src;
-    const uint64_t pitch = dp.reads[std::find(frame_of.begin(), frame_of.end(), uint32_t(f)) - frame_of.begin()].pitch;
-    ok = fr.width * elem <= std::min<uint64_t>(fr.tail, pitch) && f < 65536 &&
-         walk_encode_map(&maps[f], src, fr.width, fr.rows, pitch, elem, row_bytes / elem, kWalkGroup);
+    ok = fr.width * elem <= std::min<uint64_t>(fr.tail, fr.pitch) && f < 65536 &&
+         walk_encode_map(&maps[f], fr.src, fr.width, fr.rows, fr.pitch, elem, row_bytes / elem, kWalkGroup);
   }
   for (WalkUnit& u : units)
     for (int h = 0; h < 2; ++h) {
