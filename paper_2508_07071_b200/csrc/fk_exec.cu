@@ -474,7 +474,10 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
     const WalkCol* ct = &cols[aux[hf.z].coltab];
     const uint32_t first = 3 * s.x0 + ct[hf.x].tap, last = 3 * s.x0 + ct[hf.x + 2 * hf.n - 1].tap;
     const uint32_t wb = first & ~15u;
-    row_bytes = std::max(row_bytes, (last + 6 - wb + 15) & ~15u);
+    const uint32_t bw = (last + 6 - wb + 31) & ~31u;  // the half's box width (32-byte classes)
+    row_bytes = std::max(row_bytes, bw);
+    u.bw[h] = uint16_t(std::min(bw, 65504u));
+    ok = ok && bw <= 65504;
     u.z[h] = hf.z;
     u.bx[h] = uint16_t(wb / 2);
     u.x[h] = uint16_t(hf.x);
@@ -502,14 +505,17 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
       }
     }
   }
-  // TMA tensor maps: one per source frame (buffer, pitch), its rows [0, rows)
+  // TMA tensor maps: one per source frame (buffer, pitch) and box width class,
+  // its rows [0, rows)
   // as elements of 2, 4 or 8 bytes (the smallest whose 256-element box holds a
   // staged row) over [0, width): rows = the lowest crop bottom, width = the
   // widest crop's right edge rounded up to an element. The tensor's last
   // element of a row may extend past a crop, so that byte range must be
   // readable: every row but the frame's last has a row below it (pitch bytes),
-  // the last row its crop's tail_bytes. One map per frame keeps the TMA
-  // descriptor cache warm (one per crop missed on every copy).
+  // the last row its crop's tail_bytes. One map per frame and width class
+  // keeps the TMA descriptor cache warm (one per crop missed on every copy);
+  // per-half box widths stage only the bytes a half needs (one widest box for
+  // every half staged ~1.8x the crop bytes).
   const uint32_t elem = row_bytes <= 512 ? 2 : row_bytes <= 1024 ? 4 : 8;
   if (!ok || units.empty() || row_bytes > 256 * elem) return false;
   if (walk_smem_bytes(row_bytes, band_rows) > 200 * 1024) return false;
@@ -529,17 +535,23 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
     fr.width = std::max(fr.width, (end + elem - 1) / elem);
     ok = ok && s.pitch <= 0xffffffffull;
   }
-  std::vector<CUtensorMap> maps(frames.size());
-  for (size_t f = 0; f < frames.size() && ok; ++f) {
-    const Frame& fr = frames[f];
-    ok = fr.width * elem <= std::min<uint64_t>(fr.tail, fr.pitch) && f < 65536 &&
-         walk_encode_map(&maps[f], fr.src, fr.width, fr.rows, fr.pitch, elem, row_bytes / elem, kWalkGroup);
-  }
+  for (size_t f = 0; f < frames.size() && ok; ++f)
+    ok = frames[f].width * elem <= std::min<uint64_t>(frames[f].tail, frames[f].pitch);
+  std::map<std::pair<uint32_t, uint32_t>, uint32_t> map_at;  // (frame, box width) -> map
+  std::vector<CUtensorMap> maps;
   for (WalkUnit& u : units)
-    for (int h = 0; h < 2; ++h) {
+    for (int h = 0; h < 2 && ok; ++h) {
       u.bx[h] = uint16_t(u.bx[h] * 2 / elem);  // bx was in 2-byte elements
-      u.map[h] = uint16_t(frame_of[u.z[h]]);
       u.y0[h] = dp.reads[u.z[h]].y0;
+      const uint32_t f = frame_of[u.z[h]];
+      auto m = map_at.emplace(std::make_pair(f, uint32_t(u.bw[h])), uint32_t(maps.size())).first;
+      if (m->second == maps.size()) {
+        const Frame& fr = frames[f];
+        maps.emplace_back();
+        ok = maps.size() <= 65536 && walk_encode_map(&maps.back(), fr.src, fr.width, fr.rows, fr.pitch, elem,
+                                                     u.bw[h] / elem, kWalkGroup);
+      }
+      u.map[h] = uint16_t(m->second);
     }
   if (!ok) return false;
   // units of one source frame back to back (the frame stays L2-resident while

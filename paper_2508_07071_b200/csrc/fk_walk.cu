@@ -274,7 +274,7 @@ struct StageArgs {
   uint32_t bx0, bx1;    // box x of each half
   uint32_t y0, y1;      // TMA y of each half's source row r_first
   uint32_t two;         // half 1 present
-  uint32_t pad;
+  uint32_t tx;          // bytes a group's boxes deliver (kWalkGroup rows of each half's box width)
 };
 __host__ __device__ constexpr uint32_t walk_half_bytes(uint32_t rb) { return (kWalkGroup * rb + 127) / 128 * 128; }
 __host__ __device__ constexpr uint32_t walk_ring_bytes(uint32_t rb) { return kWalkSlots * 2 * walk_half_bytes(rb); }
@@ -314,6 +314,7 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   const uint32_t z = h ? U.z[1] : U.z[0];
   const uint32_t xh = h ? U.x[1] : U.x[0];
   const uint32_t x = xh + 2u * (h ? lane - n0 : lane);
+  const uint32_t bwl = h ? U.bw[1] : U.bw[0];  // the lane's half: staged row stride
   const WalkAux A = P.aux[z];
   // column constants. An idle lane lerps a valid column with s = c = 0 (v = 0:
   // never flagged) and stores to its warp's line of the plan's sink with a zero
@@ -366,6 +367,7 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
     t.y0 = U.y0[0] + r_first;
     t.y1 = U.y0[1] + r_first;
     t.two = U.n[1] != 0;
+    t.tx = kWalkGroup * (uint32_t(U.bw[0]) + (t.two ? uint32_t(U.bw[1]) : 0u));
     *sa = t;
   }
   // Called by the whole (converged) warp: the arguments are made warp-uniform
@@ -381,8 +383,8 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
     const uint32_t y1 = __shfl_sync(0xffffffffu, t.y1, 0) + g * kWalkGroup;
     const uint32_t mb = __shfl_sync(0xffffffffu, bar, 0) + 8 * slot;
     const uint32_t dst = __shfl_sync(0xffffffffu, ring, 0) + slot * GB;
-    const uint32_t box = kWalkGroup * RB;  // bytes one box delivers (zero-filled outside the crop)
-    tma_group(dst, m0, bx0, y0, m1, bx1, y1, mb, two ? 2 * box : box, two ? HB : 0u);
+    const uint32_t tx = __shfl_sync(0xffffffffu, t.tx, 0);  // the boxes' bytes (zero-filled outside the frame)
+    tma_group(dst, m0, bx0, y0, m1, bx1, y1, mb, tx, two ? HB : 0u);
   };
   if (lane == 0) {
 #pragma unroll
@@ -446,8 +448,8 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
     const uint32_t row = ring + slot * GB, r = r_first + g * kWalkGroup;
 #pragma unroll
     for (uint32_t q = 0; q < kWalkGroup; q += 2) {
-      visit(r + q, row + q * RB, HA, HB2);
-      visit(r + q + 1, row + (q + 1) * RB, HB2, HA);
+      visit(r + q, row + q * bwl, HA, HB2);
+      visit(r + q + 1, row + (q + 1) * bwl, HB2, HA);
     }
     __syncwarp();  // every lane is done with the slot
     if (g + kWalkSlots < ngroups) stage(g + kWalkSlots);

@@ -84,7 +84,8 @@ struct WalkUnit {
   uint16_t bx[2];       // TMA box x (in elements): the staged span starts at byte elem * bx of the frame row
   uint16_t x[2];        // first output column of each half
   uint16_t n[2];        // lanes of each half (n[1] = 0: one plane)
-  uint16_t map[2];      // tensor map (WalkPlan::maps) of each half's source frame
+  uint16_t map[2];      // tensor map (WalkPlan::maps) of each half's source frame and box width
+  uint16_t bw[2];       // box width of each half in bytes (a multiple of 32): its staged row stride
   uint16_t y_lo, y_hi;  // output rows
   uint16_t r_first, r_last;  // source rows visited (relative to y0)
   uint32_t rowtab;      // WalkRow index of output row 0
@@ -99,7 +100,7 @@ struct WalkPlan {
   const DSample* reads;     // exact-fix path (reference arithmetic)
   const float4* kz;         // per-plane constants [kz][op][lane] = (c, r_hi, r_lo, 0), input-lane order; or null
   uint32_t n_units;
-  uint32_t row_bytes;       // staged bytes per source row (the box width, 16-byte multiple)
+  uint32_t row_bytes;       // the widest box (bytes per staged row): sizes the ring
   uint32_t max_rows;        // output rows of the largest unit (fix-mask capacity)
   uint32_t elem;            // tensor-map element bytes (2, 4 or 8)
   uint64_t negz;            // kNegZero2 (fk_pack2.cuh): a product's runtime -0 addend
