@@ -467,7 +467,7 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   const uint32_t band_rows = (H + bands - 1) / bands;
   bands = (H + band_rows - 1) / band_rows;
   std::vector<WalkUnit> units;
-  uint32_t row_bytes = 16;
+  uint32_t row_bytes = 16, box_max = 16;
   // one half: plane z, columns [x, x + 2n): the staged span [2 bx, ...) of each crop row
   auto half = [&](WalkUnit& u, int h, const Half& hf) {
     const DSample& s = dp.reads[hf.z];
@@ -476,6 +476,7 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
     const uint32_t wb = first & ~15u;
     const uint32_t bw = (last + 6 - wb + 31) & ~31u;  // the half's box width (32-byte classes)
     row_bytes = std::max(row_bytes, bw);
+    box_max = std::max(box_max, bw);
     u.bw[h] = uint16_t(std::min(bw, 65504u));
     ok = ok && bw <= 65504;
     u.z[h] = hf.z;
@@ -495,6 +496,19 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
         half(u, 0, hs[i]);
         half(u, 1, two ? hs[i + 1] : hs[i]);
         if (!two) u.n[1] = 0;
+        if (two && u.z[0] == u.z[1] && u.x[1] > u.x[0]) {
+          // adjacent halves of one crop: ONE box over both spans (bw[1] = 0),
+          // in 64-byte classes; the ring's two half slots hold it
+          const uint32_t wb0 = 2u * u.bx[0], end1 = 2u * u.bx[1] + u.bw[1];
+          const uint32_t bwm = (end1 - wb0 + 63) & ~63u;
+          if (bwm <= 65504) {
+            u.bw[0] = uint16_t(bwm);
+            u.bw[1] = 0;
+            u.bx[1] = u.bx[0];
+            box_max = std::max(box_max, bwm);
+            row_bytes = std::max(row_bytes, ((bwm + 1) / 2 + 15) & ~15u);
+          }
+        }
         u.y_lo = uint16_t(y_lo);
         u.y_hi = uint16_t(y_hi);
         const uint32_t r1 = rt[y_lo].r1 & kWalkRowMask;
@@ -516,8 +530,8 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   // keeps the TMA descriptor cache warm (one per crop missed on every copy);
   // per-half box widths stage only the bytes a half needs (one widest box for
   // every half staged ~1.8x the crop bytes).
-  const uint32_t elem = row_bytes <= 512 ? 2 : row_bytes <= 1024 ? 4 : 8;
-  if (!ok || units.empty() || row_bytes > 256 * elem) return false;
+  const uint32_t elem = box_max <= 512 ? 2 : box_max <= 1024 ? 4 : 8;
+  if (!ok || units.empty() || box_max > 256 * elem) return false;
   if (walk_smem_bytes(row_bytes, band_rows) > 200 * 1024) return false;
   struct Frame { uint64_t src = 0, pitch = 0, rows = 0, width = 0, tail = ~0ull; };
   std::map<std::pair<uint64_t, uint64_t>, uint32_t> frame_at;
@@ -543,6 +557,10 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
     for (int h = 0; h < 2 && ok; ++h) {
       u.bx[h] = uint16_t(u.bx[h] * 2 / elem);  // bx was in 2-byte elements
       u.y0[h] = dp.reads[u.z[h]].y0;
+      if (u.bw[h] == 0) {  // merged into half 0's box
+        u.map[h] = u.map[0];
+        continue;
+      }
       const uint32_t f = frame_of[u.z[h]];
       auto m = map_at.emplace(std::make_pair(f, uint32_t(u.bw[h])), uint32_t(maps.size())).first;
       if (m->second == maps.size()) {

@@ -85,7 +85,8 @@ struct WalkUnit {
   uint16_t x[2];        // first output column of each half
   uint16_t n[2];        // lanes of each half (n[1] = 0: one plane)
   uint16_t map[2];      // tensor map (WalkPlan::maps) of each half's source frame and box width
-  uint16_t bw[2];       // box width of each half in bytes (a multiple of 32): its staged row stride
+  uint16_t bw[2];       // box width of each half in bytes (a multiple of 32): its staged row stride;
+                        // bw[1] = 0: adjacent halves of one crop share ONE box (bx[1] = bx[0])
   uint16_t y_lo, y_hi;  // output rows
   uint16_t r_first, r_last;  // source rows visited (relative to y0)
   uint32_t rowtab;      // WalkRow index of output row 0
