@@ -246,13 +246,14 @@ __device__ __forceinline__ uint32_t lds32(uint32_t a) {
   return v;
 }
 
-// H of one visited source row at the lane's two columns: three exact integers
-// (lanes R, G, B) per column as biased floats 2^23 + H.
-__device__ __forceinline__ void h_row(uint32_t base, const uint32_t (&w)[2], const uint32_t (&sh)[2],
-                                      const uint32_t (&wts)[2], float (&H)[2][3]) {
+// H of one visited source row at the lane's two columns (the 12-byte windows at
+// shared addresses p[0], p[1]): three exact integers (lanes R, G, B) per column
+// as biased floats 2^23 + H.
+__device__ __forceinline__ void h_row(const uint32_t (&p)[2], const uint32_t (&sh)[2], const uint32_t (&wts)[2],
+                                      float (&H)[2][3]) {
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
-    const uint32_t a = base + w[c];
+    const uint32_t a = p[c];
     const uint32_t w0 = lds32(a), w1 = lds32(a + 4), w2 = lds32(a + 8);
     const uint32_t lo = __funnelshift_r(w0, w1, sh[c]), hi = __funnelshift_r(w1, w2, sh[c]);
     const uint32_t rg = __byte_perm(lo, hi, 0x4130);  // (a_R, b_R, a_G, b_G)
@@ -433,8 +434,13 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
 
   float HA[2][3], HB2[2][3];
   // visit source row r (staged at `row`): H into Hn, then every output row it completes
-  auto visit = [&](uint32_t r, uint32_t row, float (&Hn)[2][3], float (&Hp)[2][3]) {
-    h_row(row, w, sh, wts, Hn);
+  // the lane's two tap windows in the staged row being visited: running shared
+  // addresses, one row stride per visit, a slot step per group
+  uint32_t pw[2] = {ring + w[0], ring + w[1]};
+  auto visit = [&](uint32_t r, float (&Hn)[2][3], float (&Hp)[2][3]) {
+    h_row(pw, sh, wts, Hn);
+    pw[0] += bwl;
+    pw[1] += bwl;
     while (R.r1 == r) {
       finish(Hp, Hn, R);
       R = rows[++ri];
@@ -442,17 +448,22 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   };
   // visit 0's "previous" row is row 0 itself (only a clamped row completes there)
   mbar_wait(bar, 0);
-  h_row(ring, w, sh, wts, HB2);
+  h_row(pw, sh, wts, HB2);
+  const uint32_t gstep = kWalkGroup * bwl;
   // whole groups: visits past r_last read staged rows but complete nothing (the sentinel)
   for (uint32_t g = 0; g < ngroups; ++g) {
     const uint32_t slot = g % kWalkSlots;
     mbar_wait(bar + 8 * slot, (g / kWalkSlots) & 1u);
-    const uint32_t row = ring + slot * GB, r = r_first + g * kWalkGroup;
+    const uint32_t r = r_first + g * kWalkGroup;
 #pragma unroll
     for (uint32_t q = 0; q < kWalkGroup; q += 2) {
-      visit(r + q, row + q * bwl, HA, HB2);
-      visit(r + q + 1, row + (q + 1) * bwl, HB2, HA);
+      visit(r + q, HA, HB2);
+      visit(r + q + 1, HB2, HA);
     }
+    // to the next slot's row 0 (kWalkSlots = 2: slot 0 -> 1 is + GB, 1 -> 0 is - GB)
+    const uint32_t step = (slot == 0 ? GB : 0u - GB) - gstep;
+    pw[0] += step;
+    pw[1] += step;
     __syncwarp();  // every lane is done with the slot
     if (g + kWalkSlots < ngroups) stage(g + kWalkSlots);
   }

@@ -20,6 +20,7 @@ constexpr uint32_t kWalkWarps = 4;               // warps per CTA (independent: 
 #endif
 constexpr uint32_t kWalkGroup = FK_WALK_GROUP;   // source rows per TMA box (one copy per group of visits; even)
 constexpr uint32_t kWalkSlots = 2;               // box slots per half in the ring (8-16 rows staged ahead)
+static_assert(kWalkSlots == 2, "fk_walk steps between two ring slots");
 constexpr uint32_t kWalkHalfLanes = 16;          // lanes per half-warp strip (2 output columns per lane)
 #ifndef FK_WALK_MAXROWS
 #define FK_WALK_MAXROWS 112  // 112-row bands: twice the units of whole-plane walks, a shorter tail
