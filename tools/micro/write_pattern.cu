@@ -10,14 +10,16 @@ constexpr size_t PLANE = size_t(W) * H * 4;
 
 template <int MODE>
 __global__ void __launch_bounds__(128) wp(unsigned char* out) {
-  const int cta = blockIdx.x, z = cta >> 1, band = cta & 1;
+  const int cta = blockIdx.x, band = cta & 1;
+  // MODE 4: the real pattern with CTAs in frame order (crop z uses frame z % 16, as C5's units run)
+  const int z = MODE == 4 ? ((cta >> 1) % 512) * 16 + (cta >> 1) / 512 : cta >> 1;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const float2 v = make_float2(1.0f, 2.0f);
   for (int r = 0; r < ROWS; ++r) {
     const int y = band * ROWS + r;
     for (int m = 0; m < 3; ++m) {
       unsigned char* plane = out + (size_t(z) * 3 + m) * PLANE;
-      if (MODE == 0 || MODE == 1) {  // real: warp w owns columns [64w, 64w + 64)
+      if (MODE == 0 || MODE == 1 || MODE == 4) {  // real: warp w owns columns [64w, 64w + 64)
         const int x = 64 * warp + 2 * lane;
         if (x < W) *reinterpret_cast<float2*>(plane + size_t(y) * W * 4 + x * 4) = v;
       } else if (MODE == 2) {  // CTA row-major: threads 0..111 write the 896-byte row contiguously
@@ -42,10 +44,10 @@ int main() {
   cudaEvent_t a, b;
   cudaEventCreate(&a);
   cudaEventCreate(&b);
-  const char* names[4] = {"real (warp column strips)", "real + __syncthreads per row", "CTA row-major (896 B rows)",
-                          "per-warp sequential"};
+  const char* names[5] = {"real (warp column strips)", "real + __syncthreads per row", "CTA row-major (896 B rows)",
+                          "per-warp sequential", "real, CTAs in frame order"};
   for (int rep = 0; rep < 2; ++rep)
-    for (int mode = 0; mode < 4; ++mode) {
+    for (int mode = 0; mode < 5; ++mode) {
       float best = 1e9;
       for (int it = 0; it < 5; ++it) {
         cudaMemsetAsync(flush, it, 512 << 20);
@@ -54,7 +56,8 @@ int main() {
           case 0: wp<0><<<B * 2, 128>>>(out); break;
           case 1: wp<1><<<B * 2, 128>>>(out); break;
           case 2: wp<2><<<B * 2, 128>>>(out); break;
-          default: wp<3><<<B * 2, 128>>>(out); break;
+          case 3: wp<3><<<B * 2, 128>>>(out); break;
+          default: wp<4><<<B * 2, 128>>>(out); break;
         }
         cudaEventRecord(b);
         cudaEventSynchronize(b);
