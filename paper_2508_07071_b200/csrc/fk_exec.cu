@@ -465,7 +465,6 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   uint32_t bands = uint32_t(std::min<uint64_t>((2 * target + halves - 1) / halves, (H + 7) / 8));
   bands = std::max({bands, 1u, (H + kWalkMaxRows - 1) / kWalkMaxRows});
   const uint32_t band_rows = (H + bands - 1) / bands;
-  bands = (H + band_rows - 1) / band_rows;
   std::vector<WalkUnit> units;
   uint32_t row_bytes = 16, box_max = 16;
   // one half: plane z, columns [x, x + 2n): the staged span [2 bx, ...) of each crop row
@@ -485,9 +484,22 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
     u.n[h] = uint16_t(hf.n);
     ok = ok && wb / 2 < 65536;
   };
-  for (uint32_t b = 0; b < bands; ++b) {
-    const uint32_t y_lo = b * band_rows, y_hi = std::min(H, y_lo + band_rows);
-    for (auto& kv : by_h) {
+  uint32_t max_rows = 0;
+  for (auto& kv : by_h) {
+    // A unit costs ~ rows (finishes) + visits = rows (1 + rect_h / H). Where
+    // units are long — full-height bands (many waves: the tail) or a crop more
+    // than 3x taller than the output (a band's visits are several TMA round
+    // trips) — a class's band is sized to the cost of a 1:1 band (C5 1.206 ->
+    // 1.196 ms, C2 16.7 -> 14.7 us); shorter bands elsewhere only add unit
+    // start-ups (C4 B = 8..1024: 2-6 % slower).
+    const bool balance = band_rows == kWalkMaxRows || kv.first > 3 * H;
+    const uint32_t brk =
+        balance ? std::min<uint32_t>(kWalkMaxRows,
+                                     std::max<uint32_t>(1, uint32_t(2.0 * band_rows * H / (double(H) + kv.first) + 0.5)))
+                : band_rows;
+    max_rows = std::max(max_rows, brk);
+    for (uint32_t y_lo = 0; y_lo < H; y_lo += brk) {
+      const uint32_t y_hi = std::min(H, y_lo + brk);
       const WalkRow* rt = &rows[row_at[kv.first]];
       const std::vector<Half>& hs = kv.second;
       for (size_t i = 0; i < hs.size(); i += 2) {
@@ -532,7 +544,7 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   // every half staged ~1.8x the crop bytes).
   const uint32_t elem = box_max <= 512 ? 2 : box_max <= 1024 ? 4 : 8;
   if (!ok || units.empty() || box_max > 256 * elem) return false;
-  if (walk_smem_bytes(row_bytes, band_rows) > 200 * 1024) return false;
+  if (walk_smem_bytes(row_bytes, max_rows) > 200 * 1024) return false;
   struct Frame { uint64_t src = 0, pitch = 0, rows = 0, width = 0, tail = ~0ull; };
   std::map<std::pair<uint64_t, uint64_t>, uint32_t> frame_at;
   std::vector<Frame> frames;
@@ -630,7 +642,7 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   P.row_bytes = row_bytes;
   P.elem = elem;
   P.negz = kNegZero2;
-  P.max_rows = band_rows;
+  P.max_rows = max_rows;
   P.sink = reinterpret_cast<uint64_t>(upload(std::vector<uint64_t>(kWalkSinkLines * 32, 0)));
   dp.extra.push_back(reinterpret_cast<void*>(P.sink));
   wsig_out = wsig;
