@@ -9,11 +9,11 @@
 // lanes — and a band of output rows. Bilinear is separable; the warp walks the
 // source rows the band needs, top to bottom, each visited ONCE:
 //
-//   stage   lane 0 copies kWalkGroup source rows of each half's byte span at a time
-//           into a per-warp shared-memory ring, one 2D TMA tensor copy per
-//           half (cp.async.bulk.tensor, the crop's rows as a tensor map; rows
-//           and bytes outside the crop read as zeros), completion on an
-//           mbarrier, one or two boxes ahead (no LSU traffic, no registers);
+//   stage   one elected lane copies kWalkGroup source rows at a time into a
+//           per-warp shared-memory ring: one 2D TMA tensor copy per half (or
+//           one for both halves of one crop), the frame's rows as a tensor map
+//           with a box as wide as the half needs, completion on the slot's
+//           mbarrier, one group ahead (no LSU traffic, no registers);
 //   H       each lane lerps row r horizontally at its two columns as exact
 //           integers: three 32-bit shared loads, a funnel shift to the
 //           column's byte offset, two byte_perm and three dp2a per column
@@ -21,20 +21,21 @@
 //   finish  every output row whose lower source row is r: vertical lerp of the
 //           two H rows in packed FP32 (FFMA2 over the lane's column pair), the
 //           exact-result filter, cast + chain in packed FP32, and one 8-byte
-//           store per destination plane (a warp writes 256
-//           contiguous bytes per plane).
+//           store per destination plane (a warp writes 2 x 128 contiguous
+//           bytes per plane).
 //
 // Exact-result filter. v (FP32, pixel units) differs from the exact rational
-// bilinear value R by at most 6.2e-5 on non-exact columns/rows (dp2a exact; the
-// FFMA2 vertical lerp <= 0.75 units of 1 / (K den); s and c rounded; the final
-// rounding; bound derived in DESIGN.md §4), and the reference's double result
-// differs from R by < 1e-12. So when |v - rint(v)| <= 0.5 - E (E = 2^-13) the
-// reference's nearbyint(res) is rint(v). Values outside the band are recomputed
-// by their lane in the reference's double arithmetic, op for op, and stored
-// over the fast value (same thread, program order). Where the column AND row
-// fractions are dyadic with <= 7 bits every FP32 step is exact (v == R), so the
-// check is off there (threshold 0.5) and exact ties round to even like the
-// reference's nearbyint.
+// bilinear value R by less than 6.9e-5 for out_w <= 224 (1.1e-4 for any width
+// the walk accepts) on non-exact columns/rows (dp2a exact; the FFMA2 vertical
+// lerp <= 0.75 units of 1 / (K den); s and c rounded; the final rounding;
+// derivation in DESIGN.md §4.1), and the reference's double result differs
+// from R by < 1e-12. So when |v - rint(v)| < 0.5 - E (E = 2^-13) the
+// reference's nearbyint(res) is rint(v); the kernel flags e^2 >= (0.5 - E)^2.
+// Flagged values are recomputed after the walk in the reference's double
+// arithmetic, op for op, and stored over the fast value (same thread, program
+// order). Where the column AND row fractions are dyadic with <= 7 bits every
+// FP32 step is exact (v == R), so the check is off there and exact ties round
+// to even like the reference's nearbyint.
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
