@@ -316,7 +316,9 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   const uint32_t z = h ? U.z[1] : U.z[0];
   const uint32_t xh = h ? U.x[1] : U.x[0];
   const uint32_t x = xh + 2u * (h ? lane - n0 : lane);
-  const bool h2 = h && U.bw[1] != 0;  // the lane reads the second box (else half 0's, or the merged one)
+  // the lane reads the second box (else half 0's, or the merged one); idle lanes of a one-half unit read
+  // half 0's staged bytes too (finite values: their v = 0 is never flagged)
+  const bool h2 = h && U.bw[1] != 0 && U.n[1] != 0;
   const uint32_t bwl = h2 ? U.bw[1] : U.bw[0];  // the lane's box: staged row stride
   const WalkAux A = P.aux[z];
   // column constants. An idle lane lerps a valid column with s = c = 0 (v = 0:
