@@ -59,30 +59,6 @@ __host__ __device__ constexpr bool div2(uint32_t sig, int k) { return (sig >> (k
 
 // The chain's constants for input lane m, op k, as pairs: c, and for a division
 // either (r_hi, r_lo) [two-op form] or (RN(1/c), -c) [three-op form].
-#ifndef FK_WALK_KREG
-#define FK_WALK_KREG 0  // 1: chain constants held in registers (measured slower: 1.46 vs 1.39 ms on C5)
-#endif
-#if FK_WALK_KREG
-template <uint32_t SIG>
-struct KInl {  // the chain's constants held in registers (only those the chain uses)
-  uint64_t cc[4][3], hh[4][3], ll[4][3];
-  uint64_t z;  // runtime -0 pair (fk_pack2.cuh)
-  __device__ __forceinline__ KInl(const WalkPlan& P, uint64_t negz) : z(negz) {
-#pragma unroll
-    for (int k = 0; k < 4; ++k)
-#pragma unroll
-      for (int m = 0; m < 3; ++m) {
-        const bool div = k < sig_n(SIG) && sig_fn(SIG, k) == AF_DIV;
-        cc[k][m] = k < sig_n(SIG) && !(div && (div2(SIG, k) || sig_fast(SIG, k))) ? p2::of(P.kc[k][m]) : 0;
-        hh[k][m] = div ? p2::of(P.kh[k][m]) : 0;
-        ll[k][m] = div ? p2::of(P.kl[k][m]) : 0;
-      }
-  }
-  __device__ __forceinline__ uint64_t c(int k, int m) const { return cc[k][m]; }
-  __device__ __forceinline__ uint64_t h(int k, int m) const { return hh[k][m]; }
-  __device__ __forceinline__ uint64_t l(int k, int m) const { return ll[k][m]; }
-};
-#else
 template <uint32_t SIG>
 struct KInl {
   const WalkPlan& P;
@@ -92,7 +68,6 @@ struct KInl {
   __device__ __forceinline__ uint64_t h(int k, int m) const { return p2::of(P.kh[k][m]); }
   __device__ __forceinline__ uint64_t l(int k, int m) const { return p2::of(P.kl[k][m]); }
 };
-#endif
 template <uint32_t SIG>
 struct KReg {
   uint64_t cc[4][3], hh[4][3], ll[4][3];
