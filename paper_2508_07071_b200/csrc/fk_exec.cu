@@ -319,7 +319,10 @@ WalkRow walk_row(uint32_t y, uint32_t rect_h, uint32_t out_h) {
   const bool same = iy0 == iy1;
   r.r1 = iy1 | (same ? kWalkSame : 0u) | ((same || (ny * 128) % den == 0) ? kWalkExactRow : 0u);
   r.fy = same ? 1.0f : float(double(ny) / double(den));  // clamped: both taps are row r1 (fk_walk: Ha + (Hb - Ha) 1 = Hb)
-  r.fy_ = r.fy;
+  { // the reference's double coordinate (ops.cpp:253-257 center_coord, floor): fk_walk's exact recompute
+    const double cy = ((double(y) + 0.5) * double(rect_h)) / double(out_h) - 0.5;
+    r.fyd = cy - std::floor(cy);
+  }
   return r;
 }
 
@@ -334,6 +337,11 @@ WalkCol walk_col(uint32_t x, uint32_t rect_w, uint32_t out_w) {
   const uint32_t ix1 = uint32_t(std::min(std::max<int64_t>(ix + 1, 0), maxx));
   WalkCol c{};
   c.tap = 3 * ix0;
+  c.d1 = 3 * (ix1 - ix0);
+  {
+    const double cx = ((double(x) + 0.5) * double(rect_w)) / double(out_w) - 0.5;
+    c.fx = cx - std::floor(cx);
+  }
   if (ix0 == ix1 || (nx * 128) % den == 0) {  // exact: units of 2^-14 pixel
     const uint32_t j = ix0 == ix1 ? 0u : uint32_t(nx * 16384 / den);
     c.wts = (16384u - j) | (j << 16);
@@ -435,7 +443,7 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
     if (r == row_at.end()) {
       r = row_at.emplace(s.rect_h, uint32_t(rows.size())).first;
       for (uint32_t y = 0; y < H; ++y) rows.push_back(walk_row(y, s.rect_h, H));
-      rows.push_back(WalkRow{kWalkRowMask, 0, 0.0f, 0.0f});  // sentinel: the walk reads one row ahead
+      rows.push_back(WalkRow{kWalkRowMask, 0.0f, 0.0});  // sentinel: the walk reads one row ahead
     }
     auto c = col_at.find(s.rect_w);
     if (c == col_at.end()) {

@@ -132,47 +132,49 @@ __device__ __forceinline__ float exact_lane(uint32_t a, uint32_t b, uint32_t c, 
   return float(uint32_t(__double2loint(__dadd_rn(res, 6755399441055744.0))) & 0xffu);
 }
 
-// Both columns (x, x + 1) and the three lanes of output row y of plane z,
-// recomputed exactly as the reference does (bilinear_sample in double,
-// round_clamp_u8, the chain in IEEE f32 op by op) and stored over the fast
-// values. Runs for lanes whose fast value came within E of a rounding boundary.
+// The flagged pair of output row y of lane `owner` of warp unit u — both
+// columns (x, x + 1) and the three lanes — recomputed exactly as the reference
+// does: bilinear_sample in double op for op (ops.cpp:250,283-296) with the
+// reference's own fx / fy and taps (precomputed per column / row in the walk
+// tables: no double division here), round_clamp_u8, then the chain on that u8.
+// The chain is the walk's own packed form, proven equal to the reference's IEEE
+// ops on every u8 input (host-verified divisions), so the stored values are the
+// reference's. Runs after the walk for pairs whose fast value came within E of
+// a rounding boundary; stores over the fast values (same thread, program order).
 template <uint32_t SIG, bool PERZ>
-__device__ __noinline__ void fix_pair(const WalkPlan& P, uint32_t z, uint32_t x, uint32_t y) {
-  const DSample s = P.reads[z];
-  const WalkAux A = P.aux[z];
-  const float4* kz = PERZ ? P.kz + 12ull * A.kz : nullptr;
-  const YEnt ye = dev::y_entry(s, y);
-  const uint8_t* r0 = reinterpret_cast<const uint8_t*>(s.src) + ye.r0;
-  const uint8_t* r1 = reinterpret_cast<const uint8_t*>(s.src) + ye.r1;
-  for (uint32_t c = 0; c < 2; ++c) {
-    const XEnt xe = dev::x_entry(s, x + c, 3);
-    for (int m = 0; m < 3; ++m) {
-      float v = exact_lane(__ldg(r0 + xe.o0 + m), __ldg(r0 + xe.o1 + m), __ldg(r1 + xe.o0 + m), __ldg(r1 + xe.o1 + m),
-                           xe.f, ye.f);
-#pragma unroll
-      for (int k = 0; k < sig_n(SIG); ++k) {
-        const float cst = PERZ ? __ldg(kz + 3 * k + m).x : P.kc[k][m].x;
-        switch (sig_fn(SIG, k)) {
-          case AF_MUL: v = __fmul_rn(v, cst); break;
-          case AF_ADD: v = __fadd_rn(v, cst); break;
-          case AF_SUB: v = __fsub_rn(v, cst); break;
-          default: v = __fdiv_rn(v, cst); break;
-        }
-      }
-      __stcs(reinterpret_cast<float*>(P.dst_base + A.dst[m] + uint64_t(y) * A.dpitch) + x + c, v);
-    }
-  }
-}
-
-// The flagged values of output row y of lane `owner` of warp unit u (its
-// plane and columns recomputed from the unit, as fk_walk assigns them).
-template <uint32_t SIG, bool PERZ>
-__device__ __forceinline__ void fix_owner(const WalkPlan& P, uint32_t u, uint32_t owner, uint32_t y) {
+__device__ __noinline__ void fix_owner(const WalkPlan& P, uint32_t u, uint32_t owner, uint32_t y) {
   const WalkUnit& U = P.units[u];
   const uint32_t n0 = U.n[0];
   const bool h = owner >= n0;
+  const uint32_t z = h ? U.z[1] : U.z[0];
   const uint32_t x = (h ? U.x[1] : U.x[0]) + 2u * (h ? owner - n0 : owner);
-  fix_pair<SIG, PERZ>(P, h ? U.z[1] : U.z[0], x, y);
+  const WalkAux A = P.aux[z];
+  const DSample s = P.reads[z];
+  const WalkRow R = P.rows[U.rowtab + y];
+  const WalkCol C0 = P.cols[A.coltab + x], C1 = P.cols[A.coltab + x + 1];
+  const uint32_t i1 = R.r1 & kWalkRowMask, i0 = (R.r1 & kWalkSame) ? i1 : i1 - 1u;
+  const uint8_t* r0 = reinterpret_cast<const uint8_t*>(s.src) + uint64_t(s.y0 + i0) * s.pitch + A.x3;
+  const uint8_t* r1 = reinterpret_cast<const uint8_t*>(s.src) + uint64_t(s.y0 + i1) * s.pitch + A.x3;
+  float k[2][3];
+#pragma unroll
+  for (int c = 0; c < 2; ++c) {
+    const WalkCol& C = c ? C1 : C0;
+#pragma unroll
+    for (int m = 0; m < 3; ++m)
+      k[c][m] = exact_lane(__ldg(r0 + C.tap + m), __ldg(r0 + C.tap + C.d1 + m), __ldg(r1 + C.tap + m),
+                           __ldg(r1 + C.tap + C.d1 + m), C.fx, R.fyd);
+  }
+  using KS = typename std::conditional<PERZ, KReg<SIG>, KInl<SIG>>::type;
+  const KS ks = [&]() {
+    if constexpr (PERZ) return KReg<SIG>(P.kz + 12ull * A.kz, P.negz);
+    else return KInl<SIG>(P, P.negz);
+  }();
+#pragma unroll
+  for (int m = 0; m < 3; ++m) {
+    const uint64_t o = chain2<SIG>(p2::pack(k[0][m], k[1][m]), ks, m);
+    *reinterpret_cast<float2*>(P.dst_base + A.dst[m] + uint64_t(y) * A.dpitch + 4ull * x) =
+        make_float2(p2::lo(o), p2::hi(o));
+  }
 }
 
 // ------------------------------------------------------- TMA tensor copies --

@@ -50,7 +50,8 @@ struct WalkCol {
   uint32_t wts;   // dp2a weights wa | wb << 16 (wb = 0 when both taps clamp to one column)
   float s, c;     // pixel scale of H, see above
   float thr;      // -T of the exact-result filter on an exact row: -kWalkOff2 (exact column) or -kWalkThr2
-  uint32_t pad[3];
+  uint32_t d1;    // bytes from the left to the right tap: 3, or 0 when both clamp to one column
+  double fx;      // the reference's fx (center_coord - floor, ops.cpp:259-270): the exact recompute
 };
 // One output row y of a (rect_h, out_h) table: the row completes when the walk
 // has visited source row r1 (relative to y0, clamped); r0 = r1 - 1, or r0 = r1
@@ -59,8 +60,8 @@ struct WalkCol {
 // kWalkRowMask, never visited) so the walk may read one row past out_h.
 struct WalkRow {
   uint32_t r1;    // r1 | same << 31 (r0 == r1) | exact << 30 (fy = j / 2^m, m <= 7, or same)
-  uint32_t pad;
-  float fy, fy_;  // RN(ny / den) (1 when clamped), twice: the FFMA2 operand pair
+  float fy;       // RN(ny / den) (1 when clamped)
+  double fyd;     // the reference's fy (center_coord - floor): the exact recompute
 };
 constexpr uint32_t kWalkSame = 0x80000000u;
 constexpr uint32_t kWalkExactRow = 0x40000000u;
