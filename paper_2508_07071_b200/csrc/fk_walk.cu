@@ -141,17 +141,29 @@ __device__ __forceinline__ float exact_lane(uint32_t a, uint32_t b, uint32_t c, 
 // ops on every u8 input (host-verified divisions), so the stored values are the
 // reference's. Runs after the walk for pairs whose fast value came within E of
 // a rounding boundary; stores over the fast values (same thread, program order).
+// The unit's fields the recompute needs, kept in the warp's shared memory so its
+// table loads are one round trip (no unit -> plane -> column chain).
+struct UnitFix {
+  uint32_t z[2];
+  uint32_t coltab[2];
+  uint32_t rowtab;
+  uint16_t x[2];
+  uint16_t n0, pad;
+  uint32_t pad2;
+};
+static_assert(sizeof(UnitFix) == 32, "UnitFix");
+
 template <uint32_t SIG, bool PERZ>
-__device__ __noinline__ void fix_owner(const WalkPlan& P, uint32_t u, uint32_t owner, uint32_t y) {
-  const WalkUnit& U = P.units[u];
-  const uint32_t n0 = U.n[0];
-  const bool h = owner >= n0;
-  const uint32_t z = h ? U.z[1] : U.z[0];
-  const uint32_t x = (h ? U.x[1] : U.x[0]) + 2u * (h ? owner - n0 : owner);
+__device__ __noinline__ void fix_owner(const WalkPlan& P, const UnitFix* uf, uint32_t owner, uint32_t y) {
+  const UnitFix F = *uf;
+  const bool h = owner >= F.n0;
+  const uint32_t z = h ? F.z[1] : F.z[0];
+  const uint32_t x = (h ? F.x[1] : F.x[0]) + 2u * (h ? owner - F.n0 : owner);
+  const uint32_t ct = (h ? F.coltab[1] : F.coltab[0]) + x;
   const WalkAux A = P.aux[z];
   const DSample s = P.reads[z];
-  const WalkRow R = P.rows[U.rowtab + y];
-  const WalkCol C0 = P.cols[A.coltab + x], C1 = P.cols[A.coltab + x + 1];
+  const WalkRow R = P.rows[F.rowtab + y];
+  const WalkCol C0 = P.cols[ct], C1 = P.cols[ct + 1];
   const uint32_t i1 = R.r1 & kWalkRowMask, i0 = (R.r1 & kWalkSame) ? i1 : i1 - 1u;
   const uint8_t* r0 = reinterpret_cast<const uint8_t*>(s.src) + uint64_t(s.y0 + i0) * s.pitch + A.x3;
   const uint8_t* r1 = reinterpret_cast<const uint8_t*>(s.src) + uint64_t(s.y0 + i1) * s.pitch + A.x3;
@@ -266,7 +278,7 @@ struct RowEnt {        // a WalkRow as the walk reads it: one 16-byte shared loa
 constexpr uint32_t kWalkMeta = 64;  // mbarriers + StageArgs
 static_assert(8 * kWalkSlots + sizeof(StageArgs) <= kWalkMeta, "walk meta");
 __host__ __device__ constexpr uint32_t walk_warp_bytes(uint32_t rb, uint32_t max_rows) {
-  return (walk_ring_bytes(rb) + kWalkMeta + 16 * (max_rows + 1) + 4 * max_rows + 16 + 127) / 128 * 128;
+  return (walk_ring_bytes(rb) + kWalkMeta + 16 * (max_rows + 1) + 32 + 4 * max_rows + 16 + 127) / 128 * 128;
 }
 
 // ------------------------------------------------------------------ kernel --
@@ -283,7 +295,8 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   const uint32_t bar = ring + kWalkSlots * GB;
   StageArgs* sa = reinterpret_cast<StageArgs*>(wbase + kWalkSlots * GB + 8 * kWalkSlots);
   RowEnt* rows = reinterpret_cast<RowEnt*>(wbase + kWalkSlots * GB + kWalkMeta);
-  uint32_t* fixm = reinterpret_cast<uint32_t*>(rows + P.max_rows + 1);
+  UnitFix* ufix = reinterpret_cast<UnitFix*>(rows + P.max_rows + 1);
+  uint32_t* fixm = reinterpret_cast<uint32_t*>(ufix + 1);
 
   // lane role: half h, plane z, output columns x, x + 1 (fields picked with
   // selects: a dynamic index into U would put it in local memory)
@@ -298,6 +311,17 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
   const bool h2 = h && U.bw[1] != 0 && U.n[1] != 0;
   const uint32_t bwl = h2 ? U.bw[1] : U.bw[0];  // the lane's box: staged row stride
   const WalkAux A = P.aux[z];
+  if (lane == 0 || lane == n0) {  // the recompute's unit record; each half's first lane (n0 < 32) its column table
+    if (lane == 0) {
+      ufix->z[0] = U.z[0];
+      ufix->z[1] = U.z[1];
+      ufix->rowtab = U.rowtab;
+      ufix->x[0] = U.x[0];
+      ufix->x[1] = U.x[1];
+      ufix->n0 = uint16_t(n0);
+    }
+    ufix->coltab[lane == 0 ? 0 : 1] = A.coltab;
+  }
   // column constants. An idle lane lerps a valid column with s = c = 0 (v = 0:
   // never flagged) and stores to its warp's line of the plan's sink with a zero
   // row step, so the finish carries no store predicate. (One sink line shared by
@@ -469,13 +493,13 @@ __global__ void __launch_bounds__(kWalkWarps * 32, PERZ ? 6 : FK_WALK_MINB) fk_w
           for (uint32_t t = 0; t < take; ++t) mask &= mask - 1;
           pend += take;
           if (pend == 32) {
-            fix_owner<SIG, PERZ>(P, u, my_owner, y_lo + my_row);
+            fix_owner<SIG, PERZ>(P, ufix, my_owner, y_lo + my_row);
             pend = 0;
           }
         }
       }
     }
-    if (lane < pend) fix_owner<SIG, PERZ>(P, u, my_owner, y_lo + my_row);
+    if (lane < pend) fix_owner<SIG, PERZ>(P, ufix, my_owner, y_lo + my_row);
   }
 }
 
