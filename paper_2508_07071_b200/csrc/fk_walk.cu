@@ -154,7 +154,7 @@ struct UnitFix {
 static_assert(sizeof(UnitFix) == 32, "UnitFix");
 
 template <uint32_t SIG, bool PERZ>
-__device__ __noinline__ void fix_owner(const WalkPlan& P, const UnitFix* uf, uint32_t owner, uint32_t y) {
+__device__ __forceinline__ void fix_owner(const WalkPlan& P, const UnitFix* uf, uint32_t owner, uint32_t y) {
   const UnitFix F = *uf;
   const bool h = owner >= F.n0;
   const uint32_t z = h ? F.z[1] : F.z[0];
