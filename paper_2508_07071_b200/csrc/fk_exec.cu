@@ -494,13 +494,13 @@ bool build_walk(DeviceProgram& dp, const Pipeline& p, const std::vector<DOp>& ar
   };
   uint32_t max_rows = 0;
   for (auto& kv : by_h) {
-    // A unit costs ~ rows (finishes) + visits = rows (1 + rect_h / H). Where
-    // units are long — full-height bands (many waves: the tail) or a crop more
-    // than 3x taller than the output (a band's visits are several TMA round
-    // trips) — a class's band is sized to the cost of a 1:1 band (C5 1.206 ->
-    // 1.196 ms, C2 16.7 -> 14.7 us); shorter bands elsewhere only add unit
-    // start-ups (C4 B = 8..1024: 2-6 % slower).
-    const bool balance = band_rows == kWalkMaxRows || kv.first > 3 * H;
+    // A unit costs ~ rows (finishes) + visits = rows (1 + rect_h / H). Where a
+    // crop is more than 3x taller than the output (a band's visits are several
+    // TMA round trips), its class's band is sized to the cost of a 1:1 band
+    // (C2 16.7 -> 15.2 us). Elsewhere uniform bands measure best (C5: 75-row
+    // uniform bands 1.149 ms, cost-balanced 112-row bands 1.161, balanced
+    // 80-row 1.177; C4 B = 8..1024: shorter bands only add unit start-ups).
+    const bool balance = kv.first > 3 * H;
     const uint32_t brk =
         balance ? std::min<uint32_t>(kWalkMaxRows,
                                      std::max<uint32_t>(1, uint32_t(2.0 * band_rows * H / (double(H) + kv.first) + 0.5)))
